@@ -1,0 +1,179 @@
+"""Single-shard table: the CSR HashGraph built on the GPU (mirrors core.py of the reference).
+
+`HashGraph` keeps its arrays in HBM (`offset_device` uint32[V+1],
+`keys_device` uint32/uint64[N]); the reference-facing attributes `offset`
+(int64[V+1]) and `keys` are read-only numpy copies materialised on first
+access, so code written against the reference keeps working unchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .errors import ConfigError
+from .hashing import HashFamily, family_code, hash_key, hash_range_for
+
+MASK32 = 0xFFFFFFFF
+
+
+@dataclass(frozen=True)
+class Bucket:
+    """Read-only view of the keys stored under one hash value (core.py:34-42)."""
+
+    hash_value: int
+    entries: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.entries)
+
+
+@dataclass(frozen=True)
+class BuildCounters:
+    """Keys touched by each build pass (core.py:45-55)."""
+
+    hashed: int
+    counted: int
+    placed: int
+
+    @property
+    def total(self) -> int:
+        return self.hashed + self.counted + self.placed
+
+
+class HashGraph:
+    """The CSR pair plus the parameters that produced it; immutable (core.py:58-81)."""
+
+    __slots__ = ("offset_device", "keys_device", "hash_range", "family", "load_factor", "key_bits",
+                 "_num_keys", "_offset", "_keys", "_frozen")
+
+    def __init__(self, offset_device, keys_device, hash_range: int, family, load_factor: float,
+                 key_bits: int = 32, num_keys: int | None = None):
+        object.__setattr__(self, "offset_device", offset_device)
+        object.__setattr__(self, "keys_device", keys_device)
+        object.__setattr__(self, "hash_range", int(hash_range))
+        object.__setattr__(self, "family", family)
+        object.__setattr__(self, "load_factor", float(load_factor))
+        object.__setattr__(self, "key_bits", int(key_bits))
+        object.__setattr__(self, "_num_keys", int(keys_device.numel() if num_keys is None else num_keys))
+        object.__setattr__(self, "_offset", None)
+        object.__setattr__(self, "_keys", None)
+        object.__setattr__(self, "_frozen", True)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"HashGraph is immutable (cannot set {name!r})")
+
+    @property
+    def num_keys(self) -> int:
+        return self._num_keys
+
+    @property
+    def offset(self) -> np.ndarray:
+        if self._offset is None:
+            object.__setattr__(self, "_offset", D.frozen(D.widen_u32_to_numpy(self.offset_device)))
+        return self._offset
+
+    @property
+    def keys(self) -> np.ndarray:
+        if self._keys is None:
+            object.__setattr__(self, "_keys", D.frozen(D.to_numpy_keys(self.keys_device, self.key_bits)))
+        return self._keys
+
+    def bucket(self, h: int) -> Bucket:
+        if not 0 <= h < self.hash_range:
+            raise IndexError(f"hash value {h} outside [0, {self.hash_range})")
+        lo, hi = (int(x) for x in self.offset_device[h:h + 2].cpu().numpy().view(np.uint32))
+        entries = D.to_numpy_keys(self.keys_device[lo:hi], self.key_bits)
+        return Bucket(h, D.frozen(entries))
+
+    def contains(self, key: int) -> int:
+        """Number of occurrences of `key` in the table (0 when absent)."""
+        h = hash_key(self.family, key, self.hash_range, self.key_bits)
+        entries = self.bucket(h).entries
+        mask = MASK32 if self.key_bits == 32 else (1 << 64) - 1
+        return int(np.count_nonzero(entries == entries.dtype.type(key & mask)))
+
+    def __repr__(self) -> str:
+        return (f"HashGraph(num_keys={self.num_keys}, hash_range={self.hash_range}, family={self.family!r}, "
+                f"load_factor={self.load_factor}, key_bits={self.key_bits}, device={self.keys_device.device})")
+
+
+def as_device_table(table) -> HashGraph:
+    """Accept our HashGraph or any reference-shaped table (offset/keys numpy)."""
+    if isinstance(table, HashGraph):
+        return table
+    D.require_cuda()
+    offset = np.asarray(table.offset, dtype=np.int64)
+    keys = np.asarray(table.keys)
+    key_bits = 64 if keys.dtype == np.uint64 else 32
+    if offset[-1] >= 1 << 32:
+        raise ConfigError("device tables hold fewer than 2^32 keys")
+    off_dev = D.torch().from_numpy(offset.astype(np.uint32).view(np.int32)).to(D.device())
+    keys_dev = D.to_device_keys(keys, key_bits)
+    return HashGraph(off_dev, keys_dev, table.hash_range, table.family, table.load_factor, key_bits)
+
+
+def _resolve_range(n: int, load_factor: float, hash_range) -> int:
+    if hash_range is None:
+        return hash_range_for(n, load_factor)
+    if load_factor <= 0:
+        raise ConfigError(f"load factor must be positive, got {load_factor}")
+    if hash_range < 1:
+        raise ConfigError(f"hash range must be >= 1, got {hash_range}")
+    return int(hash_range)
+
+
+def build_device(keys_dev, v: int, family, key_bits: int = 32, want_positions: bool = False):
+    """Launch the GPU build over device keys: (offset u32[v+1], edges, positions u32 | None).
+
+    Enqueue-only on the current stream."""
+    t = D.torch()
+    n = keys_dev.numel()
+    kind, seed = family_code(family)
+    offsets = t.empty(v + 1, dtype=t.int32, device=keys_dev.device)
+    edges = t.empty(n, dtype=keys_dev.dtype, device=keys_dev.device)
+    positions = t.empty(n, dtype=t.int32, device=keys_dev.device) if want_positions else None
+    ws = D.workspace(_lib.load().hg_build_workspace_size(n, v, key_bits))
+    _lib.call("hg_build", D.ptr(keys_dev), n, key_bits, kind, seed, v, D.ptr(offsets), D.ptr(edges),
+              D.ptr(positions), D.ptr(ws), ws.numel(), D.stream_ptr())
+    return offsets, edges, positions
+
+
+def build(keys, load_factor: float = 1.0, family: HashFamily = HashFamily(), worker_count: int = 1,
+          hash_range: int | None = None, key_bits: int = 32) -> HashGraph:
+    """Build a table over `keys` on the GPU (core.py:164-180).
+
+    `worker_count` is validated like the reference but has no effect: the
+    parallelism is the GPU's.  `key_bits=64` builds over uint64 keys.
+    """
+    table, _, _ = _build(keys, load_factor, family, worker_count, hash_range, key_bits, False)
+    return table
+
+
+def build_traced(keys, load_factor: float = 1.0, family: HashFamily = HashFamily(), worker_count: int = 1,
+                 hash_range: int | None = None, key_bits: int = 32):
+    """build() plus counters and positions (core.py:183-209).
+
+    positions[p] is the input index of the key stored at keys[p] (int64 numpy).
+    """
+    table, counters, pos = _build(keys, load_factor, family, worker_count, hash_range, key_bits, True)
+    positions = D.widen_u32_to_numpy(pos) if pos is not None and pos.numel() else np.zeros(0, np.int64)
+    return table, counters, positions
+
+
+def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_positions):
+    if key_bits not in (32, 64):
+        raise ConfigError(f"key_bits must be 32 or 64, got {key_bits}")
+    if not D.is_cuda_tensor(keys):
+        keys = D.coerce_host_keys(keys, key_bits)  # validate shape before range checks
+    if worker_count < 1:
+        raise ConfigError(f"worker count must be >= 1, got {worker_count}")
+    n = len(keys) if not D.is_cuda_tensor(keys) else keys.numel()
+    v = _resolve_range(n, load_factor, hash_range)
+    dk = D.to_device_keys(keys, key_bits)
+    offsets, edges, positions = build_device(dk, v, family, key_bits, want_positions)
+    table = HashGraph(offsets, edges, v, family, float(load_factor), key_bits, n)
+    return table, BuildCounters(hashed=n, counted=n, placed=n), positions

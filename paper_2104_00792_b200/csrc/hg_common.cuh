@@ -1,0 +1,195 @@
+// hg_common.cuh -- shared device/host helpers for libhashgraph_b200 (sm_100a).
+//
+// Hash family (hashing.py:77-114): murmur32 = fmix32(key ^ seed) mod V,
+// identity = key mod V.  64-bit keys (an extension; the reference truncates to
+// uint32 at core.py:84-88) use the Murmur3 fmix64 finalizer.  The reduction
+// mod V is exact: a mask for powers of two, Lemire's fastmod (M = 2^64/V + 1,
+// exact for every 32-bit numerator) otherwise.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/hashgraph_b200.h"
+
+namespace hg {
+
+// --------------------------------------------------------------------------- errors
+
+int set_error(int code, const char* fmt, ...);
+int cuda_error(cudaError_t e, const char* where);
+
+// Per-launch bookkeeping: launch counter and optional CUDA-event timing.
+void note_launch_begin(const char* name, cudaStream_t s);
+void note_launch_end(cudaStream_t s);
+
+#define HG_CHECK_CUDA(expr)                                        \
+  do {                                                             \
+    cudaError_t _e = (expr);                                       \
+    if (_e != cudaSuccess) return ::hg::cuda_error(_e, #expr);     \
+  } while (0)
+
+// Launch a kernel with bookkeeping; returns from the enclosing function on a
+// launch error.
+#define HG_LAUNCH(name, kernel, grid, block, smem, stream, ...)             \
+  do {                                                                     \
+    ::hg::note_launch_begin(name, stream);                                 \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+    cudaError_t _e = cudaGetLastError();                                   \
+    ::hg::note_launch_end(stream);                                         \
+    if (_e != cudaSuccess) return ::hg::cuda_error(_e, name);              \
+  } while (0)
+
+// --------------------------------------------------------------------------- hashing
+
+struct HashParams {
+  uint64_t v;      // hash range (>= 1)
+  uint64_t magic;  // fastmod multiplier, valid when mode == kFastmod
+  uint64_t mask;   // v - 1, valid when mode == kMask
+  uint32_t seed;
+  int kind;        // 0 murmur, 1 identity
+  int mode;        // kMask / kFastmod / kNone / kGeneric64
+};
+
+enum { kMask = 0, kFastmod = 1, kNone = 2, kGeneric64 = 3 };
+
+inline HashParams make_hash_params(int kind, uint32_t seed, uint64_t v, int key_bits) {
+  HashParams hp{};
+  hp.v = v;
+  hp.seed = seed;
+  hp.kind = kind;
+  if ((v & (v - 1)) == 0) {
+    hp.mode = kMask;
+    hp.mask = v - 1;
+  } else if (key_bits == 32 && v > 0xFFFFFFFFull) {
+    hp.mode = kNone;  // every 32-bit mixed value is already < v
+  } else if (v <= 0xFFFFFFFFull) {
+    hp.mode = kFastmod;
+    hp.magic = UINT64_MAX / v + 1;
+  } else {
+    hp.mode = kGeneric64;
+  }
+  return hp;
+}
+
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t h) {
+  h ^= h >> 33;
+  h *= 0xFF51AFD7ED558CCDull;
+  h ^= h >> 33;
+  h *= 0xC4CEB9FE1A85EC53ull;
+  h ^= h >> 33;
+  return h;
+}
+
+__device__ __forceinline__ uint32_t fastmod_u32(uint32_t x, uint64_t magic, uint32_t d) {
+  uint64_t low = magic * (uint64_t)x;
+  return (uint32_t)__umul64hi(low, (uint64_t)d);
+}
+
+__device__ __forceinline__ uint64_t mix_key(uint32_t key, const HashParams& hp) {
+  return hp.kind == HG_KIND_IDENTITY ? (uint64_t)key : (uint64_t)fmix32(key ^ hp.seed);
+}
+__device__ __forceinline__ uint64_t mix_key(uint64_t key, const HashParams& hp) {
+  return hp.kind == HG_KIND_IDENTITY ? key : fmix64(key ^ (uint64_t)hp.seed);
+}
+
+// hash(key) mod v, general (any v).
+template <typename K>
+__device__ __forceinline__ uint64_t hash_mod(K key, const HashParams& hp) {
+  uint64_t x = mix_key(key, hp);
+  switch (hp.mode) {
+    case kMask:
+      return x & hp.mask;
+    case kNone:
+      return x;
+    case kFastmod:
+      if (sizeof(K) == 4) return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
+      return x % hp.v;
+    default:
+      return x % hp.v;
+  }
+}
+
+// Bucket id for builds/queries: v <= 2^32 is enforced on the host, so the
+// result fits uint32.
+template <typename K>
+__device__ __forceinline__ uint32_t bucket_of(K key, const HashParams& hp) {
+  return (uint32_t)hash_mod(key, hp);
+}
+
+// Exact floor division of a hash value by a bin size (fastdiv for 32-bit h).
+struct DivParams {
+  uint64_t d;
+  uint64_t magic;
+  int shift;  // >= 0 when d is a power of two
+};
+
+inline DivParams make_div_params(uint64_t d) {
+  DivParams p{};
+  p.d = d;
+  p.shift = -1;
+  if ((d & (d - 1)) == 0) {
+    int s = 0;
+    while ((1ull << s) < d) s++;
+    p.shift = s;
+  } else {
+    p.magic = UINT64_MAX / d + 1;
+  }
+  return p;
+}
+
+__device__ __forceinline__ uint64_t div_by(uint64_t h, const DivParams& p) {
+  if (p.shift >= 0) return h >> p.shift;
+  if (h <= 0xFFFFFFFFull && p.d <= 0xFFFFFFFFull) return __umul64hi(p.magic, h);
+  return h / p.d;
+}
+
+// --------------------------------------------------------------------------- misc
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Simple bump allocator over a caller-provided workspace.
+struct Workspace {
+  char* base;
+  size_t cap;
+  size_t used;
+  template <typename T>
+  T* take(size_t count) {
+    used = align_up(used, 256);
+    T* p = reinterpret_cast<T*>(base + used);
+    used += count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return used <= cap; }
+};
+
+}  // namespace hg

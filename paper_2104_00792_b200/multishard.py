@@ -1,0 +1,489 @@
+"""Partitioned build across P shards (mirrors multishard.py of the reference).
+
+This module is the single-process drop-in: P shard inputs in, P local tables
+out.  All P shards live on the current GPU ("virtual shards", the analogue of
+the reference's shard threads, multishard.py:414-419), so every phase is the
+same sm_100a kernel the multi-GPU path runs:
+
+  Phase 1  hg_bin_histogram (per shard, accumulated) + hg_split_plan
+  Phase 2  hg_reorganize   (stable per-destination CSR, search-step counter)
+  Phase 3  device-to-device row gathers in ascending sender order
+  Phase 4  hg_build with the local range V_d = ceil(N_d / C)
+
+The one-process-per-GPU version over NCCL is `paper_2104_00792_b200.distributed`.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .core import BuildCounters, HashGraph, build_device
+from .errors import ConfigError
+from .hashing import HashFamily, family_code, hash_range_for
+from .query import QueryResult, QueryStageTimes, query_device
+
+PHASE_NAMES = ("partition", "preprocess", "all_to_all", "table_construction")
+
+PASS_NAMES = (
+    "hash",
+    "bin_count",
+    "dest_search",
+    "buffer_place",
+    "exchange",
+    "local_hash",
+    "local_count",
+    "local_place",
+)
+
+
+@dataclass(frozen=True)
+class ShardConfig:
+    """Build configuration; zero means "derive it" (multishard.py:53-80)."""
+
+    shards: int
+    load_factor: float = 1.0
+    bins_g: int = 0
+    family: HashFamily = HashFamily()
+    hash_range: int = 0
+
+    def __post_init__(self) -> None:
+        if self.shards < 1:
+            raise ConfigError(f"shard count must be >= 1, got {self.shards}")
+        if self.load_factor <= 0:
+            raise ConfigError(f"load factor must be positive, got {self.load_factor}")
+        if self.bins_g < 0:
+            raise ConfigError(f"bins_g must be >= 0, got {self.bins_g}")
+        if self.hash_range < 0:
+            raise ConfigError(f"hash_range must be >= 0, got {self.hash_range}")
+
+    def resolve(self, total_keys: int) -> tuple[int, int, int]:
+        """(hash_range, bins_g, bin_size) for an input of total_keys."""
+        hr = self.hash_range or hash_range_for(total_keys, self.load_factor)
+        bins = self.bins_g or max(self.shards, round(math.sqrt(hr)))
+        if bins < self.shards:
+            raise ConfigError(f"bins_g={bins} is less than shard count {self.shards}")
+        return hr, bins, -(-hr // bins)
+
+
+@dataclass(frozen=True)
+class PartitionPlan:
+    """Hash-range ownership from global bin counts (multishard.py:83-113).
+
+    Shard d owns hash values [bin_splits[d] * bin_size, bin_splits[d+1] * bin_size).
+    """
+
+    shards: int
+    hash_range: int
+    bins_g: int
+    bin_size: int
+    bin_splits: np.ndarray
+
+    def __post_init__(self) -> None:
+        s = np.asarray(self.bin_splits, dtype=np.int64)
+        object.__setattr__(self, "bin_splits", s)
+        if len(s) != self.shards + 1 or s[0] != 0 or s[-1] != self.bins_g:
+            raise ConfigError(f"malformed bin splits {s}")
+        if np.any(np.diff(s) < 0):
+            raise ConfigError(f"bin splits not monotone: {s}")
+        s.flags.writeable = False
+
+    @property
+    def boundaries(self) -> np.ndarray:
+        return self.bin_splits * self.bin_size
+
+    def shard_of(self, hashes: np.ndarray) -> np.ndarray:
+        """Destination shard of each global hash value (host helper on host arrays)."""
+        return np.searchsorted(self.boundaries, hashes, side="right") - 1
+
+    def splits_device(self):
+        return D.torch().from_numpy(np.array(self.bin_splits, dtype=np.int64)).to(D.device())
+
+
+class SendBuffers:
+    """One shard's outgoing keys as a CSR with one row per destination (multishard.py:116-134).
+
+    Held in HBM (`offsets_device` int64[P+1], `keys_device`); `offsets` /
+    `keys` / `row()` materialise numpy views for host inspection.
+    """
+
+    def __init__(self, offsets, keys, *, key_bits: int = 32, _device=None):
+        if _device is not None:
+            self.offsets_device, self.keys_device, off_host = _device
+            self._offsets = np.asarray(off_host, dtype=np.int64)
+            self.key_bits = key_bits
+            self._keys = None
+            return
+        off = np.asarray(offsets, dtype=np.int64)
+        ks = np.asarray(keys)
+        key_bits = 64 if ks.dtype == np.uint64 else 32
+        ks = ks.astype(np.uint64 if key_bits == 64 else np.uint32)
+        if off[0] != 0 or off[-1] != len(ks):
+            raise ConfigError("send buffer offsets do not cover the key array")
+        if np.any(np.diff(off) < 0):
+            raise ConfigError("send buffer offsets not monotone")
+        self._offsets = off
+        self._keys = ks
+        self.key_bits = key_bits
+        self.offsets_device = None
+        self.keys_device = D.to_device_keys(ks, key_bits)
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return self._offsets
+
+    @property
+    def keys(self) -> np.ndarray:
+        if self._keys is None:
+            self._keys = D.to_numpy_keys(self.keys_device, self.key_bits)
+        return self._keys
+
+    @property
+    def shards(self) -> int:
+        return len(self._offsets) - 1
+
+    def row(self, d: int) -> np.ndarray:
+        return self.keys[self._offsets[d]:self._offsets[d + 1]]
+
+    def row_device(self, d: int):
+        return self.keys_device[int(self._offsets[d]):int(self._offsets[d + 1])]
+
+
+@dataclass
+class ExchangeFabric:
+    """All-to-all between virtual shards on one device (multishard.py:137-166)."""
+
+    shards: int
+    posted: list = field(default_factory=list)
+    keys_moved: int = 0
+    bytes_moved: int = 0
+
+    def __post_init__(self) -> None:
+        if not self.posted:
+            self.posted = [None] * self.shards
+
+    def post(self, shard: int, buffers: SendBuffers) -> None:
+        assert buffers.shards == self.shards, "send CSR row count != shard count"
+        self.posted[shard] = buffers
+
+    def gather_device(self, shard: int):
+        """Row `shard` of every sender, ascending sender order, as one device array."""
+        rows = []
+        for s in range(self.shards):
+            sb = self.posted[s]
+            assert sb is not None, f"shard {s} has not posted its buffers"
+            rows.append(sb.row_device(shard))
+        kb = rows[0].element_size() if rows else 4
+        total = sum(r.numel() for r in rows)
+        out = D.torch().empty(total, dtype=rows[0].dtype if rows else D.torch().int32, device=D.device())
+        at = 0
+        for r in rows:  # D2D copies (cudaMemcpyAsync) on the current stream
+            if r.numel():
+                out[at:at + r.numel()].copy_(r, non_blocking=True)
+            at += r.numel()
+        self.keys_moved += total
+        self.bytes_moved += kb * total
+        return out
+
+    def gather(self, shard: int) -> np.ndarray:
+        sb = self.posted[0]
+        return D.to_numpy_keys(self.gather_device(shard), sb.key_bits if sb is not None else 32)
+
+
+@dataclass(frozen=True)
+class ShardedHashGraph:
+    """P local tables plus the plan that routes keys to them (multishard.py:169-180)."""
+
+    plan: PartitionPlan
+    shards: list
+    family: HashFamily
+    received_counts: list
+
+    @property
+    def total_keys(self) -> int:
+        return sum(self.received_counts)
+
+
+@dataclass
+class PhaseStats:
+    time_ns: int = 0
+    keys_touched: int = 0
+    search_steps: int = 0
+    bytes_exchanged: int = 0
+
+
+@dataclass
+class PhaseReport:
+    """Per-phase device times and deterministic counters (multishard.py:183-240).
+
+    Phase times are CUDA-event device times of each phase over all shards.
+    """
+
+    shards: int
+    total_keys: int
+    hash_range: int
+    bins_g: int
+    load_factor: float
+    family: HashFamily
+    phases: dict
+    passes: dict
+    search_steps: int
+    bytes_exchanged: int
+    shard_received_counts: list
+    total_time_ns: int
+    build_throughput: float
+
+    def to_json_dict(self) -> dict:
+        kind = self.family.kind
+        return {
+            "schema": "phase-report-v1",
+            "shards": self.shards,
+            "total_keys": self.total_keys,
+            "hash_range": self.hash_range,
+            "bins_g": self.bins_g,
+            "load_factor": self.load_factor,
+            "family": kind.name.lower() if hasattr(kind, "name") else str(kind),
+            "seed": self.family.seed,
+            "total_time_ns": self.total_time_ns,
+            "build_throughput_keys_per_sec": self.build_throughput,
+            "phases": {
+                name: {
+                    "time_ns": st.time_ns,
+                    "keys_touched": st.keys_touched,
+                    "search_steps": st.search_steps,
+                    "bytes_exchanged": st.bytes_exchanged,
+                }
+                for name, st in self.phases.items()
+            },
+            "passes": dict(self.passes),
+            "search_steps": self.search_steps,
+            "bytes_exchanged": self.bytes_exchanged,
+            "shard_received_counts": list(self.shard_received_counts),
+        }
+
+
+@dataclass(frozen=True)
+class AuditVerdict:
+    ok: bool
+    violations: list
+
+
+# --------------------------------------------------------------------------- device phases
+
+
+def _inputs_to_device(per_shard_inputs, key_bits=32):
+    out = []
+    for k in per_shard_inputs:
+        if not D.is_cuda_tensor(k):
+            k = D.coerce_host_keys(k, key_bits)
+        out.append(D.to_device_keys(k, key_bits))
+    return out
+
+
+def bin_histogram_device(arrays, hash_range, bins_g, bin_size, family, key_bits=32, counts=None):
+    """Phase 1 histogram of every shard into one uint64[bins_g] device array."""
+    t = D.torch()
+    if counts is None:
+        counts = t.zeros(bins_g, dtype=t.int64, device=D.device())
+    kind, seed = family_code(family)
+    for a in arrays:
+        if a.numel():
+            _lib.call("hg_bin_histogram", D.ptr(a), a.numel(), key_bits, kind, seed, hash_range, bins_g, bin_size,
+                      D.ptr(counts), D.stream_ptr())
+    return counts
+
+
+def split_plan_device(counts, bins_g, total, shards):
+    t = D.torch()
+    splits = t.empty(shards + 1, dtype=t.int64, device=D.device())
+    _lib.call("hg_split_plan", D.ptr(counts), bins_g, total, shards, D.ptr(splits), D.stream_ptr())
+    return splits
+
+
+def reorganize_device(keys_dev, hash_range, bin_size, splits_dev, shards, family, key_bits=32,
+                      want_order=False, steps=None):
+    """Phase 2 on device: (row_offsets int64[P+1] device, grouped keys, order u32 | None)."""
+    t = D.torch()
+    n = keys_dev.numel()
+    kind, seed = family_code(family)
+    rows = t.empty(shards + 1, dtype=t.int64, device=D.device())
+    grouped = t.empty(n, dtype=keys_dev.dtype, device=D.device())
+    order = t.empty(n, dtype=t.int32, device=D.device()) if want_order else None
+    ws = D.workspace(_lib.load().hg_reorganize_workspace_size(n, shards))
+    _lib.call("hg_reorganize", D.ptr(keys_dev), n, key_bits, kind, seed, hash_range, bin_size, D.ptr(splits_dev),
+              shards, D.ptr(rows), D.ptr(grouped), D.ptr(order), D.ptr(steps), D.ptr(ws), ws.numel(),
+              D.stream_ptr())
+    return rows, grouped, order
+
+
+# --------------------------------------------------------------------------- public API
+
+
+def plan_partition(per_shard_inputs, hash_range: int, bins_g: int, family: HashFamily = HashFamily()) -> PartitionPlan:
+    """Phase 1 as a standalone operation (multishard.py:266-291)."""
+    shards = len(per_shard_inputs)
+    if shards < 1:
+        raise ConfigError("need at least one shard input")
+    if hash_range < 1:
+        raise ConfigError(f"hash range must be >= 1, got {hash_range}")
+    if bins_g < shards:
+        raise ConfigError(f"bins_g={bins_g} is less than shard count {shards}")
+    bin_size = -(-hash_range // bins_g)
+    arrays = _inputs_to_device(per_shard_inputs)
+    total = sum(a.numel() for a in arrays)
+    counts = bin_histogram_device(arrays, hash_range, bins_g, bin_size, family)
+    splits = split_plan_device(counts, bins_g, total, shards)
+    return PartitionPlan(shards, hash_range, bins_g, bin_size, splits.cpu().numpy())
+
+
+def reorganize(shard_keys, plan: PartitionPlan, family: HashFamily = HashFamily()) -> SendBuffers:
+    """Phase 2 as a standalone operation: stable per-destination CSR (multishard.py:313-318)."""
+    (dk,) = _inputs_to_device([shard_keys])
+    rows, grouped, _ = reorganize_device(dk, plan.hash_range, plan.bin_size, plan.splits_device(), plan.shards,
+                                         family)
+    return SendBuffers(None, None, _device=(rows, grouped, rows.cpu().numpy()))
+
+
+def exchange(fabric: ExchangeFabric, all_buffers) -> list:
+    """Phase 3 as a standalone operation (multishard.py:321-333)."""
+    if len(all_buffers) != fabric.shards:
+        raise ConfigError(f"expected {fabric.shards} send buffers, got {len(all_buffers)}")
+    for s, sb in enumerate(all_buffers):
+        fabric.post(s, sb)
+    received = [fabric.gather(d) for d in range(fabric.shards)]
+    total_sent = sum(len(sb.keys) for sb in all_buffers)
+    assert total_sent == sum(len(r) for r in received), "exchange lost or duplicated keys"
+    return received
+
+
+def build_sharded(per_shard_inputs, config: ShardConfig, key_bits: int = 32):
+    """The four-phase build on virtual shards of one GPU (multishard.py:336-471).
+
+    Returns (ShardedHashGraph, PhaseReport)."""
+    p = config.shards
+    if len(per_shard_inputs) != p:
+        raise ConfigError(f"got {len(per_shard_inputs)} shard inputs for {p} shards")
+    t = D.require_cuda()
+    wall0 = time.perf_counter_ns()
+    arrays = _inputs_to_device(per_shard_inputs, key_bits)
+    n = sum(a.numel() for a in arrays)
+    hr, bins_g, bin_size = config.resolve(n)
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(5)]
+    steps = t.zeros(1, dtype=t.int64, device=D.device())
+
+    ev[0].record()
+    counts = bin_histogram_device(arrays, hr, bins_g, bin_size, config.family, key_bits)
+    splits = split_plan_device(counts, bins_g, n, p)
+    ev[1].record()
+    sends = []
+    for a in arrays:
+        rows, grouped, _ = reorganize_device(a, hr, bin_size, splits, p, config.family, key_bits, steps=steps)
+        sends.append((rows, grouped))
+    ev[2].record()
+    # one host sync: row sizes decide the receive buffers and the local ranges
+    rows_host = t.stack([r for r, _ in sends]).cpu().numpy() if sends else np.zeros((0, p + 1), np.int64)
+    fabric = ExchangeFabric(p)
+    for s, (rows, grouped) in enumerate(sends):
+        fabric.post(s, SendBuffers(None, None, key_bits=key_bits, _device=(rows, grouped, rows_host[s])))
+    ev3 = t.cuda.Event(enable_timing=True)
+    ev3.record()
+    received = [fabric.gather_device(d) for d in range(p)]
+    ev[3].record()
+    tables = []
+    for r in received:
+        v_d = hash_range_for(r.numel(), config.load_factor)
+        off, edges, _ = build_device(r, v_d, config.family, key_bits)
+        tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits, r.numel()))
+    ev[4].record()
+    ev[4].synchronize()
+    total_ns = time.perf_counter_ns() - wall0
+    plan = PartitionPlan(p, hr, bins_g, bin_size, splits.cpu().numpy())
+    received_counts = [int(r.numel()) for r in received]
+    assert fabric.keys_moved == n, "exchange conservation violated"
+    search_steps = int(steps.cpu().item())
+
+    def ns(a, b):
+        return int(a.elapsed_time(b) * 1e6)
+
+    phase_ns = [ns(ev[0], ev[1]), ns(ev[1], ev[2]), ns(ev3, ev[3]), ns(ev[3], ev[4])]
+    table = ShardedHashGraph(plan, tables, config.family, received_counts)
+    passes = {name: n for name in PASS_NAMES}
+    phases = {
+        "partition": PhaseStats(time_ns=phase_ns[0], keys_touched=2 * n),
+        "preprocess": PhaseStats(time_ns=phase_ns[1], keys_touched=2 * n, search_steps=search_steps),
+        "all_to_all": PhaseStats(time_ns=phase_ns[2], keys_touched=n, bytes_exchanged=fabric.bytes_moved),
+        "table_construction": PhaseStats(time_ns=phase_ns[3], keys_touched=3 * n),
+    }
+    report = PhaseReport(
+        shards=p, total_keys=n, hash_range=hr, bins_g=bins_g, load_factor=config.load_factor,
+        family=config.family, phases=phases, passes=passes, search_steps=search_steps,
+        bytes_exchanged=fabric.bytes_moved, shard_received_counts=received_counts, total_time_ns=total_ns,
+        build_throughput=(n / (total_ns / 1e9)) if (n and total_ns) else 0.0,
+    )
+    return table, report
+
+
+def query_sharded(table: ShardedHashGraph, queries, worker_count: int = 1) -> QueryResult:
+    """Count each query key's occurrences across all shards (multishard.py:474-482)."""
+    result, _ = _query_sharded(table, queries, worker_count, timed=False)
+    return result
+
+
+def query_sharded_timed(table: ShardedHashGraph, queries, worker_count: int = 1):
+    """query_sharded() plus the routing+build vs intersect split (multishard.py:485-542)."""
+    return _query_sharded(table, queries, worker_count, timed=True)
+
+
+def _query_sharded(table: ShardedHashGraph, queries, worker_count: int, timed: bool):
+    if worker_count < 1:
+        raise ConfigError(f"worker count must be >= 1, got {worker_count}")
+    t = D.require_cuda()
+    plan = table.plan
+    p = plan.shards
+    key_bits = table.shards[0].key_bits if table.shards else 32
+    (q,) = _inputs_to_device([queries], key_bits)
+    nq = q.numel()
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    rows, grouped, order = reorganize_device(q, plan.hash_range, plan.bin_size, plan.splits_device(), p, table.family,
+                                             key_bits, want_order=True)
+    rows_h = rows.cpu().numpy()
+    mult = t.zeros(nq, dtype=t.int32, device=D.device())
+    agg = t.zeros(3, dtype=t.int64, device=D.device())
+    hash_values = 0
+    ev[1].record()
+    for d, shard in enumerate(table.shards):
+        lo, hi = int(rows_h[d]), int(rows_h[d + 1])
+        hash_values += shard.hash_range
+        if hi == lo:
+            continue
+        m_d, a_d = query_device(shard, grouped[lo:hi])
+        _lib.call("hg_scatter_u32", D.ptr(m_d), D.ptr(order[lo:hi]), hi - lo, D.ptr(mult), D.stream_ptr())
+        agg += a_d
+    ev[2].record()
+    result = QueryResult(mult, agg, hash_values)
+    if not timed:
+        return result, None
+    ev[2].synchronize()
+    times = QueryStageTimes(int(ev[0].elapsed_time(ev[1]) * 1e6), int(ev[1].elapsed_time(ev[2]) * 1e6))
+    return result, times
+
+
+def work_audit(report: PhaseReport, total_keys: int, shards: int) -> AuditVerdict:
+    """Counted work against the linear-cost model (multishard.py:545-563)."""
+    violations = []
+    bound = total_keys * shards
+    if report.search_steps > bound:
+        violations.append(f"dest_search steps {report.search_steps} exceed N*P = {bound}")
+    for name in PASS_NAMES:
+        touched = report.passes.get(name)
+        if touched is None:
+            violations.append(f"missing pass counter {name!r}")
+        elif name != "dest_search" and touched > total_keys:
+            violations.append(f"pass {name!r} touched {touched} keys, bound is N = {total_keys}")
+    return AuditVerdict(ok=not violations, violations=violations)

@@ -1,0 +1,192 @@
+"""Batch querying by table intersection on the GPU (mirrors query.py of the reference).
+
+`intersect` runs the whole query (query-side table over the table's hash range
+plus the per-bucket IntersectArray) in libhashgraph_b200 and returns a
+`QueryResult` whose arrays stay in HBM until read: `multiplicities` (int64
+numpy, positional) and the aggregate counters are materialised on first
+access; `multiplicities_device` is the uint32 device array.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .core import Bucket, HashGraph, as_device_table, build_device, build_traced
+from .errors import ConfigError
+from .hashing import family_code, same_family
+
+
+class QueryResult:
+    """Per-position multiplicities plus aggregate counters (query.py:30-38)."""
+
+    __slots__ = ("multiplicities_device", "_agg_device", "hash_values", "_mult", "_agg", "_n")
+
+    def __init__(self, multiplicities_device=None, agg_device=None, hash_values: int = 0, *,
+                 multiplicities=None, matched_positions=None, total_matches=None, comparisons=None):
+        self.multiplicities_device = multiplicities_device
+        self._agg_device = agg_device
+        self.hash_values = int(hash_values)
+        self._mult = None if multiplicities is None else np.asarray(multiplicities, dtype=np.int64)
+        self._agg = None
+        if matched_positions is not None:
+            self._agg = (int(matched_positions), int(total_matches), int(comparisons))
+        self._n = (multiplicities_device.numel() if multiplicities_device is not None else len(self._mult))
+
+    @property
+    def multiplicities(self) -> np.ndarray:
+        if self._mult is None:
+            m = self.multiplicities_device
+            self._mult = D.widen_u32_to_numpy(m) if m.numel() else np.zeros(0, np.int64)
+        return self._mult
+
+    def _aggregates(self):
+        if self._agg is None:
+            a = self._agg_device.cpu().numpy().view(np.uint64)
+            self._agg = (int(a[0]), int(a[1]), int(a[2]))
+        return self._agg
+
+    @property
+    def matched_positions(self) -> int:
+        return self._aggregates()[0]
+
+    @property
+    def total_matches(self) -> int:
+        return self._aggregates()[1]
+
+    @property
+    def comparisons(self) -> int:
+        return self._aggregates()[2]
+
+    def __len__(self) -> int:
+        return self._n
+
+    def __repr__(self) -> str:
+        return f"QueryResult(n={self._n}, hash_values={self.hash_values})"
+
+
+@dataclass(frozen=True)
+class QueryStageTimes:
+    """Device-time split of a query: query-table build vs intersect (query.py:41-50)."""
+
+    table_build_ns: int
+    intersect_ns: int
+
+    @property
+    def total_ns(self) -> int:
+        return self.table_build_ns + self.intersect_ns
+
+
+@dataclass(frozen=True)
+class BucketIntersection:
+    """Result of intersecting one bucket pair (query.py:53-59)."""
+
+    counts: np.ndarray
+    total_matches: int
+    comparisons: int
+
+
+def intersect_buckets(a: Bucket, b: Bucket) -> BucketIntersection:
+    """Count, for each key in b, its occurrences in a (query.py:62-81).
+
+    A per-bucket inspection helper over two host `Bucket` views (the reference
+    uses it in tests); whole-table intersections run on the GPU.
+    """
+    if a.hash_value != b.hash_value:
+        raise ConfigError(f"bucket hash values differ: {a.hash_value} != {b.hash_value}")
+    ea, eb = np.asarray(a.entries), np.asarray(b.entries)
+    srt = np.sort(ea)
+    counts = (np.searchsorted(srt, eb, side="right") - np.searchsorted(srt, eb, side="left")).astype(np.int64)
+    return BucketIntersection(counts, int(counts.sum()), len(ea) * len(eb))
+
+
+def build_query_table(table, queries):
+    """Query-side table with the input table's hash range (query.py:84-95)."""
+    qt, _, positions = build_traced(queries, family=table.family, hash_range=table.hash_range,
+                                    key_bits=getattr(table, "key_bits", 32))
+    return qt, positions
+
+
+def _check_pair(table, query_table, worker_count):
+    if query_table.hash_range != table.hash_range:
+        raise ConfigError(f"hash ranges differ: {query_table.hash_range} != {table.hash_range}")
+    if not same_family(query_table.family, table.family):
+        raise ConfigError("hash families differ between table and query table")
+    if worker_count < 1:
+        raise ConfigError(f"worker count must be >= 1, got {worker_count}")
+    if table.hash_range > 1 << 32:
+        raise ConfigError(f"hash range {table.hash_range} exceeds the 2^32 intersection limit")
+
+
+def intersect_tables(table, query_table, positions, worker_count: int = 1) -> QueryResult:
+    """Intersect corresponding buckets of a prebuilt query table (query.py:120-179)."""
+    _check_pair(table, query_table, worker_count)
+    ta, tb = as_device_table(table), as_device_table(query_table)
+    t = D.torch()
+    if D.is_cuda_tensor(positions):
+        pos = positions.to(t.int32)
+    else:
+        pos = t.from_numpy(np.asarray(positions, dtype=np.int64).astype(np.uint32).view(np.int32)).to(D.device())
+    nb = tb.num_keys
+    mult = t.zeros(nb, dtype=t.int32, device=D.device())
+    agg = t.zeros(3, dtype=t.int64, device=D.device())
+    kind, seed = family_code(ta.family)
+    _lib.call("hg_intersect", D.ptr(ta.offset_device), D.ptr(ta.keys_device), D.ptr(tb.offset_device),
+              D.ptr(tb.keys_device), D.ptr(pos), nb, ta.key_bits, kind, seed, ta.hash_range, D.ptr(mult),
+              D.ptr(agg), D.stream_ptr())
+    return QueryResult(mult, agg, ta.hash_range)
+
+
+def query_device(table: HashGraph, queries_dev):
+    """Enqueue the whole query on the current stream; returns (mult u32, agg u64[3])."""
+    t = D.torch()
+    q = queries_dev.numel()
+    kind, seed = family_code(table.family)
+    mult = t.empty(q, dtype=t.int32, device=queries_dev.device)
+    agg = t.zeros(3, dtype=t.int64, device=queries_dev.device)
+    ws = D.workspace(_lib.load().hg_query_workspace_size(q, table.hash_range, table.key_bits))
+    _lib.call("hg_query", D.ptr(table.offset_device), D.ptr(table.keys_device), table.num_keys, D.ptr(queries_dev),
+              q, table.key_bits, kind, seed, table.hash_range, D.ptr(mult), D.ptr(agg), D.ptr(ws), ws.numel(),
+              D.stream_ptr())
+    return mult, agg
+
+
+def intersect(table, queries, worker_count: int = 1) -> QueryResult:
+    """Count each query key's occurrences in the table (query.py:182-190)."""
+    if worker_count < 1:
+        raise ConfigError(f"worker count must be >= 1, got {worker_count}")
+    ta = as_device_table(table)
+    if ta.hash_range > 1 << 32:
+        raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
+    qd = D.to_device_keys(queries, ta.key_bits)
+    mult, agg = query_device(ta, qd)
+    return QueryResult(mult, agg, ta.hash_range)
+
+
+def intersect_timed(table, queries, worker_count: int = 1):
+    """intersect() plus the build-vs-intersect split, in device nanoseconds (query.py:193-202)."""
+    if worker_count < 1:
+        raise ConfigError(f"worker count must be >= 1, got {worker_count}")
+    t = D.require_cuda()
+    ta = as_device_table(table)
+    if ta.hash_range > 1 << 32:
+        raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
+    qd = D.to_device_keys(queries, ta.key_bits)
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    q_off, q_edges, q_pos = build_device(qd, ta.hash_range, ta.family, ta.key_bits, want_positions=True)
+    ev[1].record()
+    nb = qd.numel()
+    mult = t.zeros(nb, dtype=t.int32, device=qd.device)
+    agg = t.zeros(3, dtype=t.int64, device=qd.device)
+    kind, seed = family_code(ta.family)
+    _lib.call("hg_intersect", D.ptr(ta.offset_device), D.ptr(ta.keys_device), D.ptr(q_off), D.ptr(q_edges),
+              D.ptr(q_pos), nb, ta.key_bits, kind, seed, ta.hash_range, D.ptr(mult), D.ptr(agg), D.stream_ptr())
+    ev[2].record()
+    ev[2].synchronize()
+    build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
+    inter_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
+    return QueryResult(mult, agg, ta.hash_range), QueryStageTimes(build_ns, inter_ns)
