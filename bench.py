@@ -1,0 +1,376 @@
+"""HashGraph build+query throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[4], the weak-scaling sweep, at C=1): every GPU
+owns 2^28 uniform uint32 keys drawn from {1..2^28} (SplitMix64 stream seed =
+rank, cli.py:101-107) and 2^28 queries (one stream, seed 0x51, rank slice,
+cli.py:262-266).  A step = build the table over the GPU's keys + answer its
+queries (query-side table + intersect).  N=1 runs the single-shard path; N>1
+runs the partitioned path (bin histogram all-reduce, split plan, NCCL
+all-to-all, local build; forward/backward query exchange).
+
+`value` = (keys + queries processed by all ranks) / (max-over-ranks device
+time), inputs resident in HBM.  `e2e` = the same metric through the public
+API from pinned host buffers (H2D of keys+queries and D2H of the uint32
+multiplicities inside the timed region).  `--impl reference` times the
+reference algorithm's CPU restatement (oracle/, numpy, all host threads) on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HashGraph build+query keys/sec at 1/2/4/8 B200; achieved HBM & NVLink GB/s"
+UNIT = "keys/s"
+QUERY_SEED = 0x51
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--log2-keys", type=int, default=28, help="keys (and queries) per GPU = 2^x")
+    ap.add_argument("--k", type=int, default=28, help="keys drawn from {1..2^k}")
+    ap.add_argument("--load-factor", type=float, default=1.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-log2", type=int, default=24, help="CPU baseline sample size 2^x")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- roofline bookkeeping
+
+
+def algorithmic_bytes(name: str, n: int, q: int, v: int, w: int = 4) -> float:
+    """Per-launch algorithmic bytes: the kernel's minimal
+    HBM I/O, not counting scratch."""
+    table = {
+        "hg_count": w * n,                      # read keys
+        "hg_scan": 4 * v + 4 * (v + 1),         # read counts, write offsets
+        "hg_place": 2 * w * n,                  # read keys, write edges
+        "hg_place_pos": 2 * w * q + 4 * q,      # + positions
+        "hg_intersect": 2 * w * q + 4 * q + 4 * q + w * n + 4 * (v + 1),  # q edges+pos, mult, table
+    }
+    return float(table.get(name, 0))
+
+
+def summarize_kernels(records, steps, n, q, v, peak):
+    agg = {}
+    for name, ms in records:
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += ms
+    total = sum(a[1] for a in agg.values()) or 1.0
+    rows = []
+    for name, (cnt, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        avg = ms / cnt
+        ab = algorithmic_bytes(name, n, q, v)
+        rows.append({"kernel": name, "launches": cnt, "avg_ms": avg, "share": ms / total,
+                     "achieved_gbs": (ab / (avg / 1e3) / 1e9) if ab else None})
+    top = rows[0] if rows else None
+    roof = None
+    if top:
+        ab = algorithmic_bytes(top["kernel"], n, q, v)
+        ach = ab / (top["avg_ms"] / 1e3) / 1e9 if ab else None
+        roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None, "share_of_step": top["share"],
+                "algorithmic_bytes_per_launch": ab}
+    return rows, roof
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_sample(log2: int, k: int, lf: float, workers: int):
+    """Reference algorithm (oracle restatement) on a bounded sample: build +
+    query of 2^log2 keys / queries of the bench workload's streams."""
+    import oracle as O
+
+    n = 1 << log2
+    keys = O.generate_keys(k, n, 0)
+    queries = O.generate_keys(k, n, QUERY_SEED)
+    v = O.hash_range_for(n, lf)
+    t0 = time.perf_counter()
+    off, placed, _ = O.build_csr(keys, v, workers=workers)
+    t1 = time.perf_counter()
+    O.query(off, placed, queries, workers=workers)
+    t2 = time.perf_counter()
+    return 2 * n / (t2 - t0), (t1 - t0), (t2 - t1)
+
+
+# --------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    log2 = min(args.cpu_log2, 22)
+    for _ in range(args.warmup):
+        cpu_sample(log2, args.k, args.load_factor, workers)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_sample(log2, args.k, args.load_factor, workers)[0])
+    elapsed = time.perf_counter() - t0
+    value = (2 << log2) * args.steps / elapsed
+    sample = (f"per step: build+query of 2^{log2} uint32 keys and 2^{log2} queries (k={args.k}, C={args.load_factor}) "
+              f"with the reference algorithm's numpy restatement (oracle/), worker_count={workers}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"C5 weak scaling sample: 2^{log2} keys+queries on host", "k": args.k,
+                   "load_factor": args.load_factor},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- B200 arm
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    import paper_2104_00792_b200 as hg
+    from paper_2104_00792_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = 1 << args.log2_keys
+    q = n
+    spec = hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, args.k, n, rank)
+    qspec = hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, args.k, q * world, QUERY_SEED)
+    keys = hg.generate_device(spec, 0, n)
+    queries = hg.generate_device(qspec, rank * q, q)
+    torch.cuda.synchronize()
+
+    if world > 1:
+        from paper_2104_00792_b200 import distributed as hd
+
+        cfg = hd.DistConfig(load_factor=args.load_factor)
+
+        def step():
+            table = hd.build_distributed(keys, cfg)
+            res = hd.query_distributed(table, queries)
+            return table, res
+    else:
+        def step():
+            table = hg.build(keys, args.load_factor)
+            res = hg.intersect(table, queries)
+            return table, res
+
+    v = hg.hash_range_for(n, args.load_factor)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    _lib.timing_enable(True)
+    _lib.timing_collect()
+    launches0 = _lib.launch_count()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        table, res = step()
+    e1.record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    records = _lib.timing_collect(1 << 16)
+    _lib.timing_enable(False)
+    clocks = sampler.stop() if sampler else None
+    elapsed_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        dist.barrier()
+    total_units = (n + q) * world * args.steps
+    value = total_units / (elapsed_ms / 1e3)
+
+    peak, peak_kind = measured_peak()
+    kernels, roof = summarize_kernels(records, args.steps, n, q, v, peak)
+    if roof:
+        roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback"
+        roof["traffic"] = load_traffic(roof["kernel"])
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hk = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        hq = torch.empty(q, dtype=torch.int32, pin_memory=True)
+        hk.copy_(keys.cpu())
+        hq.copy_(queries.cpu())
+        out = torch.empty(q, dtype=torch.int32, pin_memory=True)
+
+        def e2e_step():
+            if world > 1:
+                table = hd.build_distributed(hk, cfg)
+                res = hd.query_distributed(table, hq)
+            else:
+                table = hg.build(hk, args.load_factor)
+                res = hg.intersect(table, hq)
+            out.copy_(res.multiplicities_device, non_blocking=True)
+            return res
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": (n + q) * world * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 4 * (n + q), "d2h_bytes_per_step": 4 * q,
+               "ms_per_step": e2e_s / args.e2e_steps * 1e3}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        val, tb, tq = cpu_sample(args.cpu_log2, args.k, args.load_factor, workers)
+        cpu = {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": (f"2^{args.cpu_log2} keys + 2^{args.cpu_log2} queries of the same streams (k={args.k}, "
+                          f"C={args.load_factor}); build {tb:.2f} s + query {tq:.2f} s with the numpy restatement "
+                          f"of the reference (oracle/), worker_count={workers}")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": (f"C5 weak scaling: 2^{args.log2_keys} uint32 keys + 2^{args.log2_keys} queries per "
+                                f"GPU, keys from {{1..2^{args.k}}}, C={args.load_factor}"),
+                   "keys_per_gpu": n, "queries_per_gpu": q, "hash_range_per_gpu": v,
+                   "l2": "inputs (1 GiB per array) larger than the 126 MB L2",
+                   "parallelism": "single-shard" if world == 1 else f"partitioned over {world} GPUs (NCCL)"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        "kernels": kernels,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def load_traffic(kernel: str):
+    """dram bytes per launch from a committed `ncu --set full` capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

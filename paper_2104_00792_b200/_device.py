@@ -68,6 +68,14 @@ def is_cuda_tensor(x) -> bool:
     return isinstance(x, t.Tensor) and x.is_cuda
 
 
+def is_tensor(x) -> bool:
+    return isinstance(x, torch().Tensor)
+
+
+def key_count(keys) -> int:
+    return keys.numel() if is_tensor(keys) else len(keys)
+
+
 def coerce_host_keys(keys, key_bits: int = 32) -> np.ndarray:
     """core.py:84-88 -- contiguous 1-D array; 32-bit mode truncates like the reference."""
     arr = np.asarray(keys, dtype=np_key_dtype(key_bits))
@@ -90,6 +98,15 @@ def to_device_keys(keys, key_bits: int = 32):
         if keys.dtype in (t.uint64,) and key_bits == 64:
             return keys.view(t.int64).contiguous()
         return keys.to(want).contiguous()
+    if isinstance(keys, t.Tensor):  # host tensor (pinned memory copies asynchronously)
+        if keys.dim() != 1:
+            raise ConfigError(f"keys must be one-dimensional, got shape {tuple(keys.shape)}")
+        want = storage_dtype(key_bits)
+        if keys.dtype in (t.uint32, t.uint64) and keys.element_size() == (4 if key_bits == 32 else 8):
+            keys = keys.view(want)
+        elif keys.dtype != want:
+            keys = keys.to(want)
+        return keys.to(device(), non_blocking=keys.is_pinned())
     arr = coerce_host_keys(keys, key_bits)
     host = t.from_numpy(arr.view(np.int32 if key_bits == 32 else np.int64))
     return host.to(device(), non_blocking=False)

@@ -167,11 +167,11 @@ def build_traced(keys, load_factor: float = 1.0, family: HashFamily = HashFamily
 def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_positions):
     if key_bits not in (32, 64):
         raise ConfigError(f"key_bits must be 32 or 64, got {key_bits}")
-    if not D.is_cuda_tensor(keys):
+    if not D.is_tensor(keys):
         keys = D.coerce_host_keys(keys, key_bits)  # validate shape before range checks
     if worker_count < 1:
         raise ConfigError(f"worker count must be >= 1, got {worker_count}")
-    n = len(keys) if not D.is_cuda_tensor(keys) else keys.numel()
+    n = D.key_count(keys)
     v = _resolve_range(n, load_factor, hash_range)
     dk = D.to_device_keys(keys, key_bits)
     offsets, edges, positions = build_device(dk, v, family, key_bits, want_positions)

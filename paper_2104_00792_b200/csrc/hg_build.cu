@@ -6,6 +6,9 @@
 //   k_place : hash -> slot = atomicAdd(cursor[h]) -> edges[slot] = key
 //                                                    (core.py:100-101 argsort+gather)
 // and the IntersectArray query (query.py:120-179) as k_intersect.
+#include <algorithm>
+#include <cstdlib>
+
 #include "hg_common.cuh"
 
 namespace hg {
@@ -247,7 +250,8 @@ int build_impl(const K* keys, uint64_t n, HashParams hp, uint64_t v, uint32_t* o
   HG_CHECK_CUDA(cudaMemsetAsync(ticket, 0, 4, s));
   if (n) HG_LAUNCH("hg_count", k_count<K>, grid_for(n), kThreads, 0, s, keys, n, hp, counts);
   HG_LAUNCH("hg_scan", k_scan, (unsigned)tiles, kScanThreads, 0, s, counts, v, offsets, status, ticket);
-  if (n) HG_LAUNCH("hg_place", k_place<K>, grid_for(n), kThreads, 0, s, keys, n, hp, counts, edges, positions);
+  if (n) HG_LAUNCH(positions ? "hg_place_pos" : "hg_place", k_place<K>, grid_for(n), kThreads, 0, s, keys, n, hp,
+                   counts, edges, positions);
   return HG_OK;
 }
 
@@ -258,6 +262,31 @@ int intersect_impl(const uint32_t* off_a, const K* edges_a, const K* edges_b, co
   HG_LAUNCH("hg_intersect", k_intersect<K>, grid_for(n_b), kThreads, 0, s, off_a, edges_a, edges_b, pos_b,
             n_b, hp, mult, reinterpret_cast<unsigned long long*>(agg));
   return HG_OK;
+}
+
+// v2 binned path (hg_binned.cu)
+struct BinLayout {
+  int s;
+  uint32_t nbins;
+  uint32_t tile;
+  uint32_t grid;
+  uint64_t chunk;
+};
+bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L);
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query);
+template <typename K>
+int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
+                 K* edges, Workspace& ws, cudaStream_t st);
+template <typename K>
+int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st);
+
+constexpr uint64_t kBinnedMin = 1ull << 16;  // below this the 3-kernel direct path wins
+
+static bool use_binned(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L) {
+  if (n < kBinnedMin) return false;
+  if (getenv("HG_FORCE_DIRECT")) return false;
+  return binned_layout(n_table, n, v, key_bits, L);
 }
 
 }  // namespace hg
@@ -291,7 +320,12 @@ int hg_hash(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
   return HG_OK;
 }
 
-size_t hg_build_workspace_size(uint64_t n, uint64_t v, int key_bits) { return build_ws_bytes(n, v, key_bits); }
+size_t hg_build_workspace_size(uint64_t n, uint64_t v, int key_bits) {
+  size_t b = build_ws_bytes(n, v, key_bits);
+  BinLayout L;
+  if (use_binned(n, n, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(n, L, key_bits, false));
+  return b;
+}
 
 int hg_build(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* offsets,
              void* edges, uint32_t* positions, void* workspace, size_t workspace_bytes, void* stream) {
@@ -300,6 +334,12 @@ int hg_build(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed
   Workspace ws{(char*)workspace, workspace_bytes, 0};
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
+  BinLayout L;
+  if (positions == nullptr && use_binned(n, n, v, key_bits, &L)) {
+    if (key_bits == 32)
+      return binned_build<uint32_t>((const uint32_t*)keys, n, hp, v, L, offsets, (uint32_t*)edges, ws, s);
+    return binned_build<uint64_t>((const uint64_t*)keys, n, hp, v, L, offsets, (uint64_t*)edges, ws, s);
+  }
   if (key_bits == 32)
     return build_impl<uint32_t>((const uint32_t*)keys, n, hp, v, offsets, (uint32_t*)edges, positions, ws, s);
   return build_impl<uint64_t>((const uint64_t*)keys, n, hp, v, offsets, (uint64_t*)edges, positions, ws, s);
@@ -322,18 +362,30 @@ int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const uint32_t*
 
 size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits) {
   size_t kb = key_bits / 8;
-  return align_up(4 * (v + 1), 256) + align_up(kb * q, 256) + align_up(4 * q, 256) + build_ws_bytes(q, v, key_bits) + 1024;
+  size_t b = align_up(4 * (v + 1), 256) + align_up(kb * q, 256) + align_up(4 * q, 256) + build_ws_bytes(q, v, key_bits) + 1024;
+  // the binned layout depends on the table size; size for the worst case (table of v keys)
+  BinLayout L;
+  if (use_binned(v, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true));
+  return b;
 }
 
 int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries, uint64_t q,
              int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* workspace,
              size_t workspace_bytes, void* stream) {
-  (void)n_a;
   int rc = check_common(q, key_bits, kind, v);
   if (rc) return rc;
   Workspace ws{(char*)workspace, workspace_bytes, 0};
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
+  BinLayout L;
+  if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, true) <= workspace_bytes) {
+    if (agg) HG_CHECK_CUDA(cudaMemsetAsync(agg, 0, 24, s));
+    if (key_bits == 32)
+      return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)queries, q, hp, v, L, mult,
+                                    agg, ws, s);
+    return binned_query<uint64_t>(offsets_a, (const uint64_t*)edges_a, (const uint64_t*)queries, q, hp, v, L, mult,
+                                  agg, ws, s);
+  }
   size_t kb = key_bits / 8;
   uint32_t* qoff = ws.take<uint32_t>(v + 1);
   void* qedges = ws.take<char>(kb * q);

@@ -279,7 +279,7 @@ class AuditVerdict:
 def _inputs_to_device(per_shard_inputs, key_bits=32):
     out = []
     for k in per_shard_inputs:
-        if not D.is_cuda_tensor(k):
+        if not D.is_tensor(k):
             k = D.coerce_host_keys(k, key_bits)
         out.append(D.to_device_keys(k, key_bits))
     return out

@@ -183,3 +183,38 @@ def test_full_size_properties():
     assert self_res.matched_positions == 1 << 24
     _, counts = torch.unique(keys, return_counts=True)
     assert self_res.total_matches == int((counts.to(torch.int64) ** 2).sum())
+
+
+@pytest.mark.parametrize("n,dom,lf", [((1 << 20) + 3, 1 << 22, 1.0), (1 << 21, 1 << 12, 1.0), (1 << 20, 1 << 30, 0.5),
+                                      (1 << 20, 1 << 20, 4.0), (1 << 20, 1 << 20, 16.0)])
+def test_binned_and_direct_paths_agree(monkeypatch, n, dom, lf):
+    """The v2 binned kernels (default for >= 2^16 keys) and the direct Alg. 1
+    kernels (HG_FORCE_DIRECT) produce identical offsets and bucket multisets."""
+    rng = np.random.default_rng(n ^ dom)
+    keys = rng.integers(1, dom + 1, size=n, dtype=np.uint64).astype(np.uint32)
+    queries = rng.integers(1, dom + 1, size=n // 2, dtype=np.uint64).astype(np.uint32)
+    t_binned = hg.build(keys, lf)
+    r_binned = hg.intersect(t_binned, queries)
+    monkeypatch.setenv("HG_FORCE_DIRECT", "1")
+    t_direct = hg.build(keys, lf)
+    r_direct = hg.intersect(t_direct, queries)
+    monkeypatch.delenv("HG_FORCE_DIRECT")
+    assert_table_equal(t_binned, t_direct.offset, t_direct.keys)
+    assert np.array_equal(r_binned.multiplicities, r_direct.multiplicities)
+    assert (r_binned.matched_positions, r_binned.total_matches, r_binned.comparisons) == (
+        r_direct.matched_positions, r_direct.total_matches, r_direct.comparisons)
+    # and both match the oracle
+    mult = O.count_occurrences(keys, queries)
+    assert np.array_equal(r_binned.multiplicities, mult)
+
+
+def test_all_identical_keys_large():
+    """Every key in one bucket: the oversized-bin path (global counters)."""
+    n = 1 << 20
+    keys = np.full(n, 123456, dtype=np.uint32)
+    table = hg.build(keys)
+    deg = np.diff(table.offset)
+    assert deg.max() == n and deg.sum() == n
+    assert table.contains(123456) == n
+    res = hg.intersect(table, np.array([123456, 5, 123456], dtype=np.uint32))
+    assert res.multiplicities.tolist() == [n, 0, n]
