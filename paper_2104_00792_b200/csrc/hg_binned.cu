@@ -1,84 +1,100 @@
-// hg_binned.cu -- the v2 "binned" HashGraph build and query (sm_100a).
+// hg_binned.cu -- the binned HashGraph build and query for sm_100a (v3).
 //
 // Green's cache-blocked HashGraph build ("first assigns each
 // hash value to one of B_L bins ... B_L is small enough to fit in the cache")
-// mapped onto B200 shared memory.  The hash range [0, V) is cut into bins of
-// S = 2^s consecutive buckets, sized so one bin's keys plus its S counters fit
-// in one CTA's shared memory (<= 227 KB).  Every global-memory access is then
-// a coalesced stream; all random accesses (counting, ranking, placing) hit
-// shared memory.
+// mapped onto B200 shared memory.  The hash range [0, V) is cut into FINE
+// bins of 2^s consecutive buckets, sized so one fine bin's keys (~16K) plus
+// its counters fit in the shared memory of one of the two CTAs an SM runs.
+// Keys reach their fine bin through at most two partition levels of <= 128
+// sub-bins each, so every (tile, sub-bin) run written to HBM is ~128 keys or
+// longer: HBM sees long coalesced streams, all random accesses hit smem.
 //
-//   pass A  k_bin_count      per-CTA bin histogram of a contiguous input chunk
-//   pass A' k_bin_colscan    per-(CTA, bin) exclusive prefix down each column
-//           k_bin_starts     bin start offsets + list of oversized bins
-//   pass B  k_partition      tile-by-tile partition by bin, staged in smem so
-//                            each bin's run is written contiguously; cursors
-//                            persist per CTA (no global atomics); optional
-//                            slot map (input index -> partitioned slot)
-//   pass C  k_local_build    one CTA per bin: count (packed u16 smem atomics),
-//                            scan, place in smem, write offsets+edges coalesced
-//           k_local_probe    one CTA per bin: table bin CSR staged in smem,
-//                            the bin's queries probe it (IntersectArray)
-//   pass D  k_unpartition    per-query values back to input order (replays pass B's
-//                            tiles, stages each tile's bin runs in smem)
-//   slow    k_local_build_big / k_local_probe_big for bins above smem capacity
+//   A   k_hist          per-CTA level-1 counts + global fine-bin histogram
+//       k_colscan       per-(CTA, level-1 bin) write bases
+//       k_starts        fine/level-1 starts, level-2 tile table, big-bin list
+//   P1  k_part1         CTA chunk, 8K-key tiles: per-warp smem-atomic ranks,
+//                       smem staging, one contiguous run per bin
+//   P2  k_part2         the same over each level-1 bin, claiming fine-bin space
+//   C   k_local_build   one CTA per fine bin: count, scan, place in smem,
+//                       write offsets + edges
+//   Q   k_local_probe   one CTA per fine bin: the table's CSR slice staged in
+//                       smem, the bin's queries probe it (IntersectArray)
+//   R   k_unpart<2,1>   query answers back to input order: each tile's runs
+//                       are pulled into smem and read back through a u16 map
 //
-// The result equals Alg. 1's: offsets exact, each bucket
-// the same multiset (core.py:12-14 leaves the in-bucket order unspecified).
-#include "hg_common.cuh"
+// Results equal Alg. 1's: offsets exact, every bucket the
+// same multiset (core.py:12-14 leaves the in-bucket order unspecified).
+#include "hg_binned.cuh"
 
 namespace hg {
 
-constexpr int kBT = 1024;                 // threads per CTA in the binned kernels
-constexpr int kMaxBinsLog = 13;           // bins per pass B (smem cursors)
-constexpr int kSLog = 15;                 // max buckets per bin
-constexpr uint32_t kProbeCap = 38 * 1024; // table keys per bin handled in smem (pass C probe)
+constexpr int kT = 512;          // threads per CTA; two CTAs per SM
+constexpr int kW = kT / 32;      // warps per CTA
+constexpr int kSub = 128;        // max bins per partition level (7-bit ballots)
+constexpr int kSubBits = 7;
+constexpr uint32_t kMaxFine = 16384;
 
-struct BinLayout {
-  int s;           // log2 buckets per bin
-  uint32_t nbins;  // ceil(v / 2^s)
-  uint32_t tile;   // pass B tile (keys)
-  uint32_t grid;   // CTAs of pass A / B (one chunk each)
-  uint64_t chunk;  // keys per chunk (multiple of tile)
+template <typename K>
+struct TileShape {
+  static constexpr int kTile = sizeof(K) == 4 ? 8192 : 4096;  // 32 KB staged
+  static constexpr int kKPT = kTile / kT;                     // 16 / 8 keys per thread
 };
 
-// Choose s so a bin holds ~2^15 keys: S * n / v ~= 32768.
+template <typename K>
+struct LocalShape {
+  static constexpr int kKPT = sizeof(K) == 4 ? 38 : 19;
+  static constexpr uint32_t kCap = kKPT * kT;  // keys per fine bin handled in smem
+};
+
+
+static int ceil_log2(uint32_t x) {
+  int b = 0;
+  while ((1u << b) < x) b++;
+  return b;
+}
+
 static int pick_s(uint64_t n, uint64_t v) {
   double per_bucket = v ? (double)n / (double)v : 1.0;
-  int s = kSLog;
-  while (s > 8 && per_bucket * (double)(1ull << s) > 36000.0) s--;
+  int s = 14;
+  while (s > 6 && per_bucket * (double)(1ull << s) > 17000.0) s--;
   return s;
 }
 
-// n_table sizes the bins (a bin's table keys must fit shared memory); n_items
-// (keys being partitioned) sizes the per-CTA chunks.
+// n_table sizes the fine bins (a bin's table keys must fit smem); n sizes the chunks.
 bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L) {
   if (v > (1ull << 32)) return false;
-  int s = pick_s(n_table, v);
-  uint64_t nb = (v + (1ull << s) - 1) >> s;
-  if (nb > (1ull << kMaxBinsLog)) return false;
+  const int s = pick_s(n_table, v);
+  const uint64_t F = (v + (1ull << s) - 1) >> s;
+  if (F > kMaxFine) return false;
   L->s = s;
-  L->nbins = (uint32_t)nb;
-  L->tile = key_bits == 32 ? 32768u : 16384u;  // == TileShape<K>::kTile
-  L->grid = (uint32_t)num_sms();
-  uint64_t per = (n + L->grid - 1) / L->grid;
+  L->nfine = (uint32_t)F;
+  L->two_level = F > (uint64_t)kSub;
+  L->group = L->two_level ? kSub : 1;
+  L->nb1 = (uint32_t)((F + L->group - 1) / L->group);
+  L->bits1 = ceil_log2(L->nb1);
+  L->shift1 = s + (L->two_level ? kSubBits : 0);
+  L->tile = key_bits == 32 ? 8192u : 4096u;  // == TileShape<K>::kTile
+  L->grid = (uint32_t)num_sms() * 2;
+  const uint64_t per = (n + L->grid - 1) / L->grid;
   L->chunk = (per + L->tile - 1) / L->tile * L->tile;
   if (L->chunk == 0) L->chunk = L->tile;
+  L->ntiles1 = (n + L->tile - 1) / L->tile;
+  L->max_tiles2 = L->ntiles1 + L->nb1 + 1;
   return true;
 }
 
 template <typename K>
-__device__ __forceinline__ uint32_t bin_of(K key, const HashParams& hp, int s) {
+__device__ __forceinline__ uint32_t fine_of(K key, const HashParams& hp, int s) {
   return bucket_of(key, hp) >> s;
 }
 
-// In-place exclusive scan of n (<= 16 * blockDim) uint32 values in smem.
-// Returns the total to every thread.  Caller syncs before (data ready).
+// --------------------------------------------------------------------------- block helpers
+
+// In-place exclusive scan of n (<= 32 * blockDim) uint32 in smem; returns total.
 __device__ uint32_t block_exscan(uint32_t* a, uint32_t n) {
   __shared__ uint32_t s_w[32];
   const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = threadIdx.x * per;
-  const uint32_t hi = min(lo + per, n);
+  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, n);
   uint32_t sum = 0;
   for (uint32_t i = lo; i < hi; i++) sum += a[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -111,14 +127,12 @@ __device__ uint32_t block_exscan(uint32_t* a, uint32_t n) {
   return total;
 }
 
-// Same for n packed uint16 counters stored two per word (word i holds values
-// 2i (low half) and 2i+1 (high half)); totals must stay below 65536.
-__device__ uint32_t block_exscan_u16(uint32_t* w16, uint32_t nvals) {
+// Same over n packed uint16 counters (two per word); totals stay < 65536.
+__device__ void block_exscan_u16(uint32_t* w16, uint32_t nvals) {
   __shared__ uint32_t s_w[32];
   const uint32_t nwords = (nvals + 1) / 2;
   const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = threadIdx.x * per;
-  const uint32_t hi = min(lo + per, nwords);
+  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, nwords);
   uint32_t sum = 0;
   for (uint32_t i = lo; i < hi; i++) {
     uint32_t x = w16[i];
@@ -144,7 +158,6 @@ __device__ uint32_t block_exscan_u16(uint32_t* w16, uint32_t nvals) {
   }
   __syncthreads();
   uint32_t run = (warp ? s_w[warp - 1] : 0u) + inc - sum;
-  const uint32_t total = s_w[nw - 1];
   for (uint32_t i = lo; i < hi; i++) {
     uint32_t x = w16[i];
     uint32_t a = run, b = run + (x & 0xFFFFu);
@@ -152,121 +165,6 @@ __device__ uint32_t block_exscan_u16(uint32_t* w16, uint32_t nvals) {
     run = b + (x >> 16);
   }
   __syncthreads();
-  return total;
-}
-
-// --------------------------------------------------------------------------- pass A
-
-template <typename K>
-__global__ void __launch_bounds__(kBT)
-k_bin_count(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nbins, uint64_t chunk,
-            uint32_t* __restrict__ M) {
-  extern __shared__ uint32_t s_cnt[];
-  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) s_cnt[i] = 0;
-  __syncthreads();
-  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
-  const uint64_t hi = min(n, lo + chunk);
-  if (sizeof(K) == 4 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
-    const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
-    const uint64_t nv = (hi - lo) / 4;
-    for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
-      uint4 q = __ldcs(p + i);
-      atomicAdd(s_cnt + bin_of((K)q.x, hp, s), 1u);
-      atomicAdd(s_cnt + bin_of((K)q.y, hp, s), 1u);
-      atomicAdd(s_cnt + bin_of((K)q.z, hp, s), 1u);
-      atomicAdd(s_cnt + bin_of((K)q.w, hp, s), 1u);
-    }
-    for (uint64_t i = lo + nv * 4 + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(s_cnt + bin_of(keys[i], hp, s), 1u);
-  } else {
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(s_cnt + bin_of(keys[i], hp, s), 1u);
-  }
-  __syncthreads();
-  uint32_t* row = M + (uint64_t)blockIdx.x * nbins;
-  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) row[i] = s_cnt[i];
-}
-
-// Thread per bin: exclusive prefix of the bin's counts over CTAs (in place);
-// the column total goes to totals[b].
-__global__ void k_bin_colscan(uint32_t* __restrict__ M, uint32_t G, uint32_t nbins, uint32_t* __restrict__ totals) {
-  uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nbins) return;
-  uint32_t run = 0;
-  for (uint32_t g = 0; g < G; g++) {
-    uint32_t c = M[(uint64_t)g * nbins + b];
-    M[(uint64_t)g * nbins + b] = run;
-    run += c;
-  }
-  totals[b] = run;
-}
-
-// One CTA: bin starts (exclusive scan of totals, bin_start[nbins] = total) and
-// the list of bins whose key count exceeds `cap`.
-__global__ void __launch_bounds__(kBT)
-k_bin_starts(const uint32_t* __restrict__ totals, uint32_t nbins, uint32_t cap, uint32_t* __restrict__ bin_start,
-             uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
-  extern __shared__ uint32_t s_a[];
-  __shared__ uint32_t s_big;
-  if (threadIdx.x == 0) s_big = 0;
-  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) {
-    uint32_t t = totals[i];
-    s_a[i] = t;
-    if (big_list && t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
-  }
-  __syncthreads();
-  uint32_t total = block_exscan(s_a, nbins);
-  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) bin_start[i] = s_a[i];
-  if (threadIdx.x == 0) {
-    bin_start[nbins] = total;
-    if (big_count) *big_count = s_big;
-  }
-}
-
-// --------------------------------------------------------------------------- register tiles
-
-// A CTA tile of TILE keys held in registers, KPT = TILE / kBT per thread.
-// Full, 16-byte-aligned tiles load with 128-bit vector loads (element k of a
-// thread is ((k / VPL) * kBT + tid) * VPL + k % VPL); ragged tiles load
-// element k * kBT + tid.  Both mappings are coalesced.
-template <typename K>
-struct TileShape {
-  static constexpr int kTile = sizeof(K) == 4 ? 32768 : 16384;
-  static constexpr int kKPT = kTile / kBT;
-  static constexpr int kVPL = 16 / sizeof(K);
-};
-
-template <typename K, int KPT>
-__device__ __forceinline__ uint32_t tile_elem(int k, bool vec) {
-  constexpr int VPL = 16 / sizeof(K);
-  return vec ? (uint32_t)(((k / VPL) * kBT + threadIdx.x) * VPL + k % VPL) : (uint32_t)(k * kBT + threadIdx.x);
-}
-
-template <typename K, int KPT>
-__device__ __forceinline__ bool load_tile(const K* __restrict__ src, uint32_t m, K (&kv)[KPT]) {
-  constexpr int VPL = 16 / sizeof(K);
-  const bool vec = (m == (uint32_t)KPT * kBT) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  if (vec) {
-    const uint4* p = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-    for (int l = 0; l < KPT / VPL; l++) {
-      uint4 q = __ldcs(p + l * kBT + threadIdx.x);
-      const K* qk = reinterpret_cast<const K*>(&q);
-#pragma unroll
-      for (int j = 0; j < VPL; j++) kv[l * VPL + j] = qk[j];
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < KPT; k++) {
-      uint32_t e = k * kBT + threadIdx.x;
-      kv[k] = e < m ? src[e] : K(0);
-    }
-  }
-  return vec;
-}
-
-__device__ __forceinline__ uint32_t get16(const uint32_t* p, int k) { return (p[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu; }
-__device__ __forceinline__ void set16(uint32_t* p, int k, uint32_t v) {
-  if (k & 1) p[k >> 1] = (p[k >> 1] & 0xFFFFu) | (v << 16);
-  else p[k >> 1] = (p[k >> 1] & 0xFFFF0000u) | (v & 0xFFFFu);
 }
 
 // Inclusive max-scan of n (<= 32 * blockDim) uint32 in smem, in place.
@@ -280,7 +178,7 @@ __device__ void block_maxscan(uint32_t* a, uint32_t n) {
   uint32_t inc = mx;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc = max(inc, y);
   }
   if (lane == 31) s_w[warp] = inc;
@@ -289,15 +187,15 @@ __device__ void block_maxscan(uint32_t* a, uint32_t n) {
     uint32_t w = lane < nw ? s_w[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w = max(w, y);
     }
     if (lane < nw) s_w[lane] = w;
   }
   __syncthreads();
   uint32_t run = warp ? s_w[warp - 1] : 0u;
-  uint32_t y = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane > 0) run = max(run, y);
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane > 0) run = max(run, prev);
   for (uint32_t i = lo; i < hi; i++) {
     run = max(run, a[i]);
     a[i] = run;
@@ -305,203 +203,464 @@ __device__ void block_maxscan(uint32_t* a, uint32_t n) {
   __syncthreads();
 }
 
-// --------------------------------------------------------------------------- pass B
+__device__ __forceinline__ uint32_t get16(const uint32_t* p, uint32_t k) { return (p[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu; }
 
-// Partition a CTA's contiguous chunk tile by tile.  Per tile: bins of the
-// register-held keys -> smem histogram -> tile offsets -> keys staged in smem
-// grouped by bin -> each bin's run written contiguously at the CTA's cursor.
-// kSlot also records, per input key, its staged position inside its tile
-// (pmap, uint16), which the reverse pass uses to restore query order.
-template <typename K, bool kSlot>
-__global__ void __launch_bounds__(kBT, 1)
-k_partition(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nbins, uint64_t chunk,
-            const uint32_t* __restrict__ M, const uint32_t* __restrict__ bin_start, K* __restrict__ out,
-            uint16_t* __restrict__ pmap) {
+// Tile loads: full 16-byte-aligned tiles use 128-bit loads (element of key k
+// = ((k / VPL) * kT + tid) * VPL + k % VPL); ragged tiles use k * kT + tid.
+template <typename K>
+__device__ __forceinline__ uint32_t tile_elem(int k, bool vec) {
+  constexpr int VPL = 16 / sizeof(K);
+  return vec ? (uint32_t)(((k / VPL) * kT + threadIdx.x) * VPL + k % VPL) : (uint32_t)(k * kT + threadIdx.x);
+}
+
+template <typename K, int KPT>
+__device__ __forceinline__ bool load_tile(const K* __restrict__ src, uint32_t m, K (&kv)[KPT]) {
+  constexpr int VPL = 16 / sizeof(K);
+  const bool vec = (m == (uint32_t)KPT * kT) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  if (vec) {
+    const uint4* p = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int l = 0; l < KPT / VPL; l++) {
+      uint4 q = __ldcs(p + l * kT + threadIdx.x);
+      const K* qk = reinterpret_cast<const K*>(&q);
+#pragma unroll
+      for (int j = 0; j < VPL; j++) kv[l * VPL + j] = qk[j];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KPT; k++) {
+      const uint32_t e = k * kT + threadIdx.x;
+      kv[k] = e < m ? src[e] : K(0);
+    }
+  }
+  return vec;
+}
+
+// --------------------------------------------------------------------------- pass A
+
+template <typename K>
+__global__ void __launch_bounds__(kT)
+k_hist(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nfine, uint32_t group, uint32_t nb1,
+       uint64_t chunk, uint32_t* __restrict__ M, uint32_t* __restrict__ fine_cnt) {
+  extern __shared__ uint32_t s_h[];
+  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  const uint64_t hi = min(n, lo + chunk);
+  if (sizeof(K) == 4 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
+    const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
+    const uint64_t nv = (hi - lo) / 4;
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) q[u] = __ldcs(p + i + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        atomicAdd(s_h + fine_of((K)q[u].x, hp, s), 1u);
+        atomicAdd(s_h + fine_of((K)q[u].y, hp, s), 1u);
+        atomicAdd(s_h + fine_of((K)q[u].z, hp, s), 1u);
+        atomicAdd(s_h + fine_of((K)q[u].w, hp, s), 1u);
+      }
+    }
+    for (; i < nv; i += blockDim.x) {
+      uint4 q = __ldcs(p + i);
+      atomicAdd(s_h + fine_of((K)q.x, hp, s), 1u);
+      atomicAdd(s_h + fine_of((K)q.y, hp, s), 1u);
+      atomicAdd(s_h + fine_of((K)q.z, hp, s), 1u);
+      atomicAdd(s_h + fine_of((K)q.w, hp, s), 1u);
+    }
+    for (uint64_t j = lo + nv * 4 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of(keys[j], hp, s), 1u);
+  } else {
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of(keys[j], hp, s), 1u);
+  }
+  __syncthreads();
+  uint32_t* row = M + (uint64_t)blockIdx.x * nb1;
+  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) {
+    uint32_t sum = 0;
+    const uint32_t f1 = min((c + 1) * group, nfine);
+    for (uint32_t f = c * group; f < f1; f++) sum += s_h[f];
+    row[c] = sum;
+  }
+  for (uint32_t f = threadIdx.x; f < nfine; f += blockDim.x)
+    if (s_h[f]) atomicAdd(fine_cnt + f, s_h[f]);
+}
+
+// Thread per level-1 bin: exclusive prefix down the CTA column (in place).
+__global__ void k_colscan(uint32_t* __restrict__ M, uint32_t G, uint32_t nb1) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb1) return;
+  uint32_t run = 0;
+  for (uint32_t g = 0; g < G; g++) {
+    const uint32_t c = M[(uint64_t)g * nb1 + b];
+    M[(uint64_t)g * nb1 + b] = run;
+    run += c;
+  }
+}
+
+// One CTA: fine starts (F+1), level-1 starts (nb1+1), level-2 tile prefix
+// (nb1+1; tp[nb1] = level-2 tile count), fine cursors (= fine starts) and the
+// list of fine bins above `cap` keys.
+__global__ void __launch_bounds__(1024)
+k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, uint32_t nb1, uint32_t tile,
+         uint32_t cap, uint32_t* __restrict__ fine_start, uint32_t* __restrict__ c_start, uint32_t* __restrict__ tp,
+         uint32_t* __restrict__ fine_cursor, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+  extern __shared__ uint32_t s_a[];  // nfine + nb1 + 1
+  __shared__ uint32_t s_big;
+  uint32_t* s_t = s_a + nfine;
+  if (threadIdx.x == 0) s_big = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
+    const uint32_t t = fine_cnt[i];
+    s_a[i] = t;
+    if (t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
+  }
+  __syncthreads();
+  const uint32_t total = block_exscan(s_a, nfine);
+  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
+    fine_start[i] = s_a[i];
+    fine_cursor[i] = s_a[i];
+  }
+  if (threadIdx.x == 0) {
+    fine_start[nfine] = total;
+    *big_count = s_big;
+  }
+  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) {
+    const uint32_t a = s_a[c * group];
+    const uint32_t b = (c + 1) * group < nfine ? s_a[(c + 1) * group] : total;
+    c_start[c] = a;
+    s_t[c] = (b - a + tile - 1) / tile;
+  }
+  if (threadIdx.x == 0) c_start[nb1] = total;
+  __syncthreads();
+  const uint32_t ntiles = block_exscan(s_t, nb1);
+  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) tp[c] = s_t[c];
+  if (threadIdx.x == 0) tp[nb1] = ntiles;
+}
+
+// --------------------------------------------------------------------------- partition
+
+template <typename K>
+struct PartSmem {
+  K staged[TileShape<K>::kTile];
+  uint32_t wcnt[kW][kSub];  // per-warp counts -> per-warp slot bases
+  uint32_t toff[kSub + 1];  // tile offsets per bin
+  uint32_t dst[kSub];       // global write base per bin
+  uint32_t tp[kSub + 1];    // level-2 tile prefix (P2 only)
+};
+
+// Rank a register tile by bin and stage it grouped by bin in smem.  Each key
+// takes its rank from one atomic on its warp's private bin counter (the rank
+// stays in registers); a per-bin prefix over warps then gives every key its
+// staged slot.  Afterwards s.toff holds the tile offsets.  pmap (optional)
+// receives each key's staged position, indexed by its tile element.
+template <typename K, int KPT>
+__device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT], const uint32_t (&bp)[KPT / 4],
+                                               uint32_t m, bool vec, uint32_t nb, uint16_t* __restrict__ pmap) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t b = lane; b < nb; b += 32) s.wcnt[warp][b] = 0;
+  __syncwarp();
+  uint32_t rk[KPT / 2];  // 16-bit ranks, two per register
+#pragma unroll
+  for (int k = 0; k < KPT; k++) {
+    const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
+    uint32_t r = 0;
+    if (tile_elem<K>(k, vec) < m) r = atomicAdd(&s.wcnt[warp][b], 1u);
+    if (k & 1) rk[k >> 1] |= r << 16; else rk[k >> 1] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kW; w++) {
+      const uint32_t c = s.wcnt[w][threadIdx.x];
+      s.wcnt[w][threadIdx.x] = run;
+      run += c;
+    }
+    s.toff[threadIdx.x] = run;
+  }
+  __syncthreads();
+  const uint32_t total = block_exscan(s.toff, nb);
+  if (threadIdx.x == 0) s.toff[nb] = total;
+  if (threadIdx.x < nb) {
+    const uint32_t base = s.toff[threadIdx.x];
+#pragma unroll
+    for (int w = 0; w < kW; w++) s.wcnt[w][threadIdx.x] += base;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KPT; k++) {
+    const uint32_t e = tile_elem<K>(k, vec);
+    if (e < m) {
+      const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
+      const uint32_t slot = s.wcnt[warp][b] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
+      s.staged[slot] = kv[k];
+      if (pmap) pmap[e] = (uint16_t)slot;
+    }
+  }
+  __syncthreads();
+}
+
+// Copy each bin's staged run to out[dst[b] + position in run]: warp per bin.
+template <typename K>
+__device__ __forceinline__ void write_runs(const PartSmem<K>& s, uint32_t nb, K* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t b = warp; b < nb; b += kW) {
+    const uint32_t lo = s.toff[b], hi = s.toff[b + 1];
+    K* d = out + ((int64_t)s.dst[b] - (int64_t)lo);
+    for (uint32_t j = lo + lane; j < hi; j += 32) d[j] = s.staged[j];
+  }
+}
+
+// Level 1: CTA chunk tiles, bin = bucket >> shift1, deterministic bases
+// (column-scanned per-CTA counts).  Query mode also records the u16 staged
+// position of every key (pmap) and each tile's offsets (meta, nb+1 words).
+template <typename K, bool kQuery>
+__global__ void __launch_bounds__(kT, 2)
+k_part1(const K* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int bits1, uint32_t nb1, uint64_t chunk,
+        const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, K* __restrict__ out,
+        uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
   extern __shared__ __align__(16) unsigned char s_raw[];
-  uint32_t* R = reinterpret_cast<uint32_t*>(s_raw);  // tile counts -> offsets -> running
-  uint32_t* cur = R + nbins + 1;                     // per-bin output cursor
-  K* staged = reinterpret_cast<K*>(s_raw + (((2 * nbins + 1) * 4 + 15) & ~15u));
+  PartSmem<K>& s = *reinterpret_cast<PartSmem<K>*>(s_raw);
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;
   const uint64_t hi = min(n, lo + chunk);
-  const uint32_t* row = M + (uint64_t)blockIdx.x * nbins;
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] = bin_start[b] + row[b];
-
+  const uint32_t* row = M + (uint64_t)blockIdx.x * nb1;
+  if (threadIdx.x < nb1) s.dst[threadIdx.x] = c_start[threadIdx.x] + row[threadIdx.x];
   for (uint64_t t0 = lo; t0 < hi; t0 += TS::kTile) {
     const uint32_t m = (uint32_t)min((uint64_t)TS::kTile, hi - t0);
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) R[b] = 0;
     K kv[KPT];
     const bool vec = load_tile<K, KPT>(keys + t0, m, kv);
-    uint32_t bp[KPT / 2];
-    __syncthreads();
+    uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
-      const bool ok = tile_elem<K, KPT>(k, vec) < m;
-      const uint32_t b = ok ? bin_of(kv[k], hp, s) : 0xFFFFu;
-      if (k & 1) bp[k >> 1] |= b << 16; else bp[k >> 1] = b;
-      if (ok) atomicAdd(R + b, 1u);
+      const uint32_t b = (uint32_t)(bucket_of(kv[k], hp) >> shift1);
+      if ((k & 3) == 0) bp[k >> 2] = 0;
+      bp[k >> 2] |= (b & 0xFFu) << ((k & 3) * 8);
+    }
+    __syncthreads();  // previous tile fully written out
+    rank_and_stage<K, KPT>(s, kv, bp, m, vec, nb1, kQuery ? pmap + t0 : nullptr);
+    write_runs<K>(s, nb1, out);
+    if (kQuery)
+      for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) meta[(t0 / TS::kTile) * (nb1 + 1) + i] = s.toff[i];
+    __syncthreads();
+    if (threadIdx.x < nb1) s.dst[threadIdx.x] += s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
+  }
+}
+
+// Level 2: tiles of each level-1 bin, sub-bin = fine & 127, space claimed per
+// (tile, fine bin) from the fine cursors.  Query mode records pmap (indexed in
+// level-1 order) and meta = [128 claims | 129 tile offsets] per tile.
+template <typename K, bool kQuery>
+__global__ void __launch_bounds__(kT, 2)
+k_part2(const K* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
+        const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, K* __restrict__ out,
+        uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
+  using TS = TileShape<K>;
+  constexpr int KPT = TS::kKPT;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  PartSmem<K>& s = *reinterpret_cast<PartSmem<K>*>(s_raw);
+  for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) s.tp[i] = tp_g[i];
+  __syncthreads();
+  const uint32_t ntiles = s.tp[nb1];
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint32_t a = 0, z = nb1;  // level-1 bin c: tp[c] <= t < tp[c+1]
+    while (z - a > 1) {
+      const uint32_t mid = (a + z) >> 1;
+      if (s.tp[mid] <= t) a = mid; else z = mid;
+    }
+    const uint32_t c = a;
+    const uint32_t t0 = c_start[c] + (t - s.tp[c]) * TS::kTile;
+    const uint32_t m = min((uint32_t)TS::kTile, c_start[c + 1] - t0);
+    K kv[KPT];
+    const bool vec = load_tile<K, KPT>(in + t0, m, kv);
+    uint32_t bp[KPT / 4];
+#pragma unroll
+    for (int k = 0; k < KPT; k++) {
+      const uint32_t b = (uint32_t)(bucket_of(kv[k], hp) >> s_log) & (kSub - 1);
+      if ((k & 3) == 0) bp[k >> 2] = 0;
+      bp[k >> 2] |= b << ((k & 3) * 8);
     }
     __syncthreads();
-    block_exscan(R, nbins);
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] -= R[b];
+    rank_and_stage<K, KPT>(s, kv, bp, m, vec, kSub, kQuery ? pmap + t0 : nullptr);
+    if (threadIdx.x < kSub) {
+      const uint32_t cnt = s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
+      s.dst[threadIdx.x] = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
+      if (kQuery) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
+    }
+    if (kQuery)
+      for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
     __syncthreads();
+    write_runs<K>(s, kSub, out);
+  }
+}
+
+// Reverse of a partition level for per-query uint32 values.  Level 2: tiles
+// from the level-2 tile table, run bases from meta; level 1: each CTA replays
+// its chunk's tiles with cursors from the column-scanned counts.  Runs are
+// pulled into smem in staged order, then out[i] = staged[pmap[i]].
+template <int kLevel>
+__global__ void __launch_bounds__(kT, 2)
+k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
+         const uint32_t* __restrict__ meta, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
+         const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
+  constexpr int VPT = 8192 / kT;  // staged values per thread
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw);  // tile <= 8192
+  uint32_t* toff = staged + 8192;                         // kSub + 1
+  uint32_t* base = toff + kSub + 1;                       // kSub
+  uint32_t* tps = base + kSub;                            // kSub + 1
+  uint64_t lo = 0, hi = 0;
+  uint32_t ntiles = 0;
+  if (kLevel == 1) {
+    lo = (uint64_t)blockIdx.x * chunk;
+    hi = min(n, lo + chunk);
+    if (threadIdx.x < nb) base[threadIdx.x] = c_start[threadIdx.x] + M[(uint64_t)blockIdx.x * nb + threadIdx.x];
+  } else {
+    for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) tps[i] = tp_g[i];
+    __syncthreads();
+    ntiles = tps[nb];
+  }
+  const uint32_t nbb = kLevel == 1 ? nb : kSub;
+  for (uint64_t it = (kLevel == 1 ? lo : blockIdx.x);; it += (kLevel == 1 ? tile : gridDim.x)) {
+    uint32_t m;
+    uint64_t t0, tix;
+    if (kLevel == 1) {
+      if (it >= hi) break;
+      t0 = it;
+      m = (uint32_t)min((uint64_t)tile, hi - it);
+      tix = it / tile;
+    } else {
+      if (it >= ntiles) break;
+      const uint32_t t = (uint32_t)it;
+      uint32_t a = 0, z = nb;
+      while (z - a > 1) {
+        const uint32_t mid = (a + z) >> 1;
+        if (tps[mid] <= t) a = mid; else z = mid;
+      }
+      t0 = c_start[a] + (t - tps[a]) * tile;
+      m = min(tile, c_start[a + 1] - (uint32_t)t0);
+      tix = t;
+    }
+    __syncthreads();
+    if (kLevel == 1) {
+      for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) toff[i] = meta[tix * (nb + 1) + i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < kSub; i += blockDim.x) base[i] = meta[tix * (2 * kSub + 1) + i];
+      for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) toff[i] = meta[tix * (2 * kSub + 1) + kSub + i];
+    }
+    __syncthreads();
+    {
+      // warp w gathers staged positions [w*VPT*32, (w+1)*VPT*32): find the bin
+      // of its first position once, then each lane walks forward (runs are
+      // ~tile/nb long, so a lane crosses at most a few run starts)
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const uint32_t j0 = (uint32_t)warp * VPT * 32;
+      uint32_t lo_b = 0, hi_b = nbb;  // last b with toff[b] <= j0
+      while (hi_b - lo_b > 1) {
+        const uint32_t mid = (lo_b + hi_b) >> 1;
+        if (toff[mid] <= j0) lo_b = mid; else hi_b = mid;
+      }
+      uint32_t b = lo_b;
+      uint32_t v[VPT];
 #pragma unroll
-    for (int k = 0; k < KPT; k++) {
-      const uint32_t b = get16(bp, k);
-      if (b != 0xFFFFu) {
-        const uint32_t slot = atomicAdd(R + b, 1u);
-        staged[slot] = kv[k];
-        if (kSlot) pmap[t0 + tile_elem<K, KPT>(k, vec)] = (uint16_t)slot;
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t j = j0 + k * 32 + lane;
+        uint32_t x = 0;
+        if (j < m) {
+          while (toff[b + 1] <= j) b++;
+          x = vals[(int64_t)base[b] - (int64_t)toff[b] + j];
+        }
+        v[k] = x;
+      }
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t j = j0 + k * 32 + lane;
+        if (j < m) staged[j] = v[k];
       }
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-      const K key = staged[j];
-      out[cur[bin_of(key, hp, s)] + j] = key;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) out[t0 + i] = staged[pmap[t0 + i]];
+    if (kLevel == 1) {
+      __syncthreads();
+      if (threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] += R[b];
   }
 }
 
-// Reverse of k_partition for per-query values: CTA g replays its chunk's
-// tiles (same tiling, same cursors), rebuilds each tile's bin runs, pulls the
-// runs of `vals_bo` (bin-ordered) into smem staged order, and writes
-// out[i] = staged[pmap[i]] in input order.  Every global access is coalesced
-// per run or per tile.
+// --------------------------------------------------------------------------- C: local build
+
+// One CTA per fine bin (two CTAs per SM): keys in registers, packed-u16 smem
+// counters, scan, place, then offsets and edges leave as coalesced streams.
+// `src` may alias `edges` (each CTA reads its whole range before writing it).
 template <typename K>
-__global__ void __launch_bounds__(kBT, 1)
-k_unpartition(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nbins, uint64_t chunk,
-              const uint32_t* __restrict__ M, const uint32_t* __restrict__ bin_start,
-              const uint32_t* __restrict__ vals_bo, const uint16_t* __restrict__ pmap, uint32_t* __restrict__ out) {
-  using TS = TileShape<K>;
-  constexpr int KPT = TS::kKPT;
-  constexpr int VPT = 32768 / kBT;  // staged values per thread (u32 tile of up to 32K)
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  uint32_t* R = reinterpret_cast<uint32_t*>(s_raw);
-  uint32_t* cur = R + nbins + 1;
-  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + (((2 * nbins + 1) * 4 + 15) & ~15u));
-  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
-  const uint64_t hi = min(n, lo + chunk);
-  const uint32_t* row = M + (uint64_t)blockIdx.x * nbins;
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] = bin_start[b] + row[b];
-
-  for (uint64_t t0 = lo; t0 < hi; t0 += TS::kTile) {
-    const uint32_t m = (uint32_t)min((uint64_t)TS::kTile, hi - t0);
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) R[b] = 0;
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) staged[j] = 0;
-    K kv[KPT];
-    const bool vec = load_tile<K, KPT>(keys + t0, m, kv);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < KPT; k++)
-      if (tile_elem<K, KPT>(k, vec) < m) atomicAdd(R + bin_of(kv[k], hp, s), 1u);
-    __syncthreads();
-    const uint32_t total = block_exscan(R, nbins);
-    if (threadIdx.x == 0) R[nbins] = total;
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] -= R[b];
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x)
-      if (R[b + 1] > R[b]) staged[R[b]] = b;  // run starts
-    __syncthreads();
-    block_maxscan(staged, m);  // staged[j] = bin of staged position j
-    uint32_t v[VPT];
-#pragma unroll
-    for (int k = 0; k < VPT; k++) {
-      const uint32_t j = k * kBT + threadIdx.x;
-      v[k] = j < m ? vals_bo[cur[staged[j]] + j] : 0u;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < VPT; k++) {
-      const uint32_t j = k * kBT + threadIdx.x;
-      if (j < m) staged[j] = v[k];
-    }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) out[t0 + j] = staged[pmap[t0 + j]];
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) cur[b] += R[b + 1];
-  }
-}
-
-// --------------------------------------------------------------------------- pass C: build
-
-template <typename K>
-struct BuildShape {
-  static constexpr int kKPT = sizeof(K) == 4 ? 38 : 19;
-  static constexpr uint32_t kCap = kKPT * kBT;
-};
-
-// One CTA per bin: the bin's keys (<= kCap) are held in registers; counting
-// and ranking use packed uint16 smem counters (one atomic each), offsets and
-// edges leave as coalesced streams.
-template <typename K>
-__global__ void __launch_bounds__(kBT, 1)
-k_local_build(const K* __restrict__ part, const uint32_t* __restrict__ bin_start, uint32_t nbins, HashParams hp,
-              int s, uint64_t v, uint32_t* __restrict__ offsets, K* __restrict__ edges) {
-  constexpr int KPT = BuildShape<K>::kKPT;
+__global__ void __launch_bounds__(kT, 2)
+k_local_build(const K* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s, uint64_t v,
+              uint32_t* __restrict__ offsets, K* edges) {
+  constexpr int KPT = LocalShape<K>::kKPT;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
-  uint32_t* c16 = reinterpret_cast<uint32_t*>(s_raw);  // S/2 packed u16 counters
-  K* staged = reinterpret_cast<K*>(c16 + S / 2);
-  const uint32_t b = blockIdx.x;
-  const uint32_t lo = bin_start[b], hi = bin_start[b + 1];
+  uint32_t* c16 = reinterpret_cast<uint32_t*>(s_raw);  // S/2 words
+  K* staged = reinterpret_cast<K*>(s_raw + (S / 2) * 4);
+  const uint32_t f = blockIdx.x;
+  const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
   const uint32_t cnt = hi - lo;
-  const uint64_t first = (uint64_t)b << s;
+  const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
-  if (b == nbins - 1 && threadIdx.x == 0) offsets[v] = hi;
-  if (cnt > (uint32_t)KPT * kBT) return;  // k_local_build_big owns this bin
+  if (f == nfine - 1 && threadIdx.x == 0) offsets[v] = hi;
+  if (cnt > LocalShape<K>::kCap) return;  // k_local_build_big
   K kv[KPT];
 #pragma unroll
   for (int k = 0; k < KPT; k++) {
-    const uint32_t j = k * kBT + threadIdx.x;
-    kv[k] = j < cnt ? part[lo + j] : K(0);
+    const uint32_t j = k * kT + threadIdx.x;
+    kv[k] = j < cnt ? src[lo + j] : K(0);
   }
   for (uint32_t i = threadIdx.x; i < (nb + 1) / 2; i += blockDim.x) c16[i] = 0;
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < KPT; k++) {
-    if (k * kBT + threadIdx.x < cnt) {
+  for (int k = 0; k < KPT; k++)
+    if (k * kT + threadIdx.x < cnt) {
       const uint32_t l = bucket_of(kv[k], hp) - (uint32_t)first;
       atomicAdd(c16 + (l >> 1), 1u << ((l & 1) * 16));
     }
-  }
   __syncthreads();
   block_exscan_u16(c16, nb);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = lo + get16(c16, i);
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < KPT; k++) {
-    if (k * kBT + threadIdx.x < cnt) {
+  for (int k = 0; k < KPT; k++)
+    if (k * kT + threadIdx.x < cnt) {
       const uint32_t l = bucket_of(kv[k], hp) - (uint32_t)first;
       const uint32_t sh = (l & 1) * 16;
       const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sh);
       staged[(old >> sh) & 0xFFFFu] = kv[k];
     }
-  }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) edges[lo + j] = staged[j];
 }
 
-// Oversized bins: global-memory counters (one S-sized scratch per CTA).
+// Fine bins above the smem capacity: global-memory counters (one 2^s scratch
+// per CTA).  When `copy` is set the bin is first copied from `edges` into
+// `src` (same offsets) so placement can overwrite edges.
 template <typename K>
-__global__ void __launch_bounds__(kBT)
-k_local_build_big(const K* __restrict__ part, const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ big_list,
+__global__ void __launch_bounds__(1024)
+k_local_build_big(K* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
                   const uint32_t* __restrict__ big_count, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ scratch,
-                  uint32_t* __restrict__ offsets, K* __restrict__ edges) {
+                  uint32_t* __restrict__ offsets, K* edges) {
   const uint32_t S = 1u << s;
   uint32_t* cnt = scratch + (uint64_t)blockIdx.x * S;
   __shared__ uint32_t s_w[32];
   for (uint32_t k = blockIdx.x; k < *big_count; k += gridDim.x) {
-    const uint32_t b = big_list[k];
-    const uint32_t lo = bin_start[b], hi = bin_start[b + 1];
-    const uint64_t first = (uint64_t)b << s;
+    const uint32_t f = big_list[k];
+    const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
+    const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
+    if (copy)
+      for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) src[j] = edges[j];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x)
-      atomicAdd(cnt + (bucket_of(part[j], hp) - (uint32_t)first), 1u);
+    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(cnt + (bucket_of(src[j], hp) - (uint32_t)first), 1u);
     __syncthreads();
     const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
     const uint32_t a0 = threadIdx.x * per, a1 = min(a0 + per, nb);
@@ -526,22 +685,21 @@ k_local_build_big(const K* __restrict__ part, const uint32_t* __restrict__ bin_s
     __syncthreads();
     uint32_t run = lo + (warp ? s_w[warp - 1] : 0u) + inc - sum;
     for (uint32_t i = a0; i < a1; i++) {
-      uint32_t x = cnt[i];
+      const uint32_t x = cnt[i];
       cnt[i] = run;
       offsets[first + i] = run;
       run += x;
     }
     __syncthreads();
     for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-      K key = part[j];
-      uint32_t slot = atomicAdd(cnt + (bucket_of(key, hp) - (uint32_t)first), 1u);
-      edges[slot] = key;
+      const K key = src[j];
+      edges[atomicAdd(cnt + (bucket_of(key, hp) - (uint32_t)first), 1u)] = key;
     }
     __syncthreads();
   }
 }
 
-// --------------------------------------------------------------------------- pass C: probe
+// --------------------------------------------------------------------------- Q: probe
 
 __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint64_t comps, unsigned long long* agg) {
 #pragma unroll
@@ -557,68 +715,70 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
   }
 }
 
-// One CTA per bin: the table's CSR slice for the bin (local uint16 offsets +
-// edges) is staged in smem; the bin's queries (register batches) probe it
-// with IntersectArray semantics (count of equal keys in the bucket,
-// PAPER.md:62-72) and write their counts in bin order.  Table slices above the
-// smem capacity are probed in global memory instead.
+// One CTA per fine bin: the table's CSR slice (uint16 local offsets + edges)
+// staged in smem; the bin's queries probe it with IntersectArray semantics
+// (count of equal keys in the bucket; comparisons += bucket
+// degree, query.py:153-155) and write counts in partitioned order.  Slices
+// above the smem capacity are probed in global memory.
 template <typename K>
-__global__ void __launch_bounds__(kBT, 1)
+__global__ void __launch_bounds__(kT, 2)
 k_local_probe(const uint32_t* __restrict__ t_off, const K* __restrict__ t_edges, const K* __restrict__ qpart,
-              const uint32_t* __restrict__ qbin_start, HashParams hp, int s, uint64_t v, uint32_t cap,
-              uint32_t* __restrict__ mult_bo, unsigned long long* __restrict__ agg) {
+              const uint32_t* __restrict__ q_start, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ mult_bo,
+              unsigned long long* __restrict__ agg) {
   constexpr int QPT = 16;
+  constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
   uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);
   K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 1) + 15) & ~15u));
-  const uint32_t b = blockIdx.x;
-  const uint32_t qlo = qbin_start[b], qhi = qbin_start[b + 1];
+  const uint32_t f = blockIdx.x;
+  const uint32_t qlo = q_start[f], qhi = q_start[f + 1];
   if (qlo == qhi) return;
-  const uint64_t first = (uint64_t)b << s;
+  const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
-  const bool in_smem = thi - tlo <= cap;
+  const uint32_t tn = thi - tlo;
+  const bool in_smem = tn <= kCap;
   if (in_smem) {
-    for (uint32_t i0 = 0; i0 <= nb; i0 += 8 * kBT) {
+    for (uint32_t i0 = 0; i0 <= nb; i0 += 8 * kT) {
       uint32_t x[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        uint32_t i = i0 + k * kBT + threadIdx.x;
+        const uint32_t i = i0 + k * kT + threadIdx.x;
         x[k] = i <= nb ? t_off[first + i] : 0u;
       }
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        uint32_t i = i0 + k * kBT + threadIdx.x;
+        const uint32_t i = i0 + k * kT + threadIdx.x;
         if (i <= nb) off16[i] = (uint16_t)(x[k] - tlo);
       }
     }
-    for (uint32_t j0 = 0; j0 < thi - tlo; j0 += 8 * kBT) {
+    for (uint32_t j0 = 0; j0 < tn; j0 += 8 * kT) {
       K x[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        uint32_t j = j0 + k * kBT + threadIdx.x;
-        x[k] = j < thi - tlo ? t_edges[tlo + j] : K(0);
+        const uint32_t j = j0 + k * kT + threadIdx.x;
+        x[k] = j < tn ? t_edges[tlo + j] : K(0);
       }
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        uint32_t j = j0 + k * kBT + threadIdx.x;
-        if (j < thi - tlo) tedges[j] = x[k];
+        const uint32_t j = j0 + k * kT + threadIdx.x;
+        if (j < tn) tedges[j] = x[k];
       }
     }
   }
   __syncthreads();
   uint64_t matched = 0, total = 0, comps = 0;
-  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kBT) {
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
     K qv[QPT];
 #pragma unroll
     for (int k = 0; k < QPT; k++) {
-      uint32_t j = q0 + k * kBT + threadIdx.x;
+      const uint32_t j = q0 + k * kT + threadIdx.x;
       qv[k] = j < qhi ? qpart[j] : K(0);
     }
 #pragma unroll
     for (int k = 0; k < QPT; k++) {
-      uint32_t j = q0 + k * kBT + threadIdx.x;
+      const uint32_t j = q0 + k * kT + threadIdx.x;
       if (j < qhi) {
         const K q = qv[k];
         const uint32_t h = bucket_of(q, hp);
@@ -645,70 +805,113 @@ k_local_probe(const uint32_t* __restrict__ t_off, const K* __restrict__ t_edges,
 
 // --------------------------------------------------------------------------- host drivers
 
-static size_t partition_smem(const BinLayout& L, int key_bits) {
-  return (size_t)(((2 * L.nbins + 1) * 4 + 15) & ~15u) + (size_t)32768 * 4;  // staged: 32K u32 / 16K u64
-  (void)key_bits;
+static size_t part_smem(int key_bits) {
+  return key_bits == 32 ? sizeof(PartSmem<uint32_t>) : sizeof(PartSmem<uint64_t>);
 }
-static uint32_t caps_for(int key_bits, uint32_t cap) { return key_bits == 32 ? cap : cap / 2; }
-
-static size_t build_smem(const BinLayout& L, int key_bits) {
-  return (size_t)(1u << L.s) / 2 * 4 + (size_t)(key_bits == 32 ? BuildShape<uint32_t>::kCap * 4 : BuildShape<uint64_t>::kCap * 8);
+static size_t local_smem(int s, int key_bits) {
+  return (size_t)(1u << s) / 2 * 4 + (key_bits == 32 ? LocalShape<uint32_t>::kCap * 4 : LocalShape<uint64_t>::kCap * 8);
 }
-static size_t probe_smem(const BinLayout& L, int key_bits) {
-  return (size_t)((2 * ((1u << L.s) + 1) + 15) & ~15u) + (size_t)caps_for(key_bits, kProbeCap) * (key_bits / 8);
+static size_t probe_smem(int s, int key_bits) {
+  return (size_t)((2 * ((1u << s) + 1) + 15) & ~15u) +
+         (key_bits == 32 ? LocalShape<uint32_t>::kCap * 4 : LocalShape<uint64_t>::kCap * 8);
 }
+static size_t unpart_smem() { return (8192 + 3 * kSub + 2) * 4; }
 
 size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query) {
-  size_t kb = key_bits / 8;
+  const size_t kb = key_bits / 8;
   size_t b = 0;
-  b += align_up((size_t)L.grid * L.nbins * 4, 256);  // M
-  b += align_up((size_t)L.nbins * 4, 256);           // totals
-  b += align_up((size_t)(L.nbins + 1) * 4, 256);     // bin starts
-  b += align_up((size_t)L.nbins * 4, 256) + 256;     // big list + count
-  b += align_up(n * kb, 256);                        // partitioned keys
-  if (query) b += align_up(n * 2, 256) + align_up(n * 4, 256);  // pmap + bin-ordered multiplicities
-  else b += align_up((size_t)num_sms() * (1u << L.s) * 4, 256);  // big-bin scratch
-  return b + 1024;
+  b += align_up((size_t)L.grid * L.nb1 * 4, 256);        // M
+  b += 4 * align_up(((size_t)L.nfine + 1) * 4, 256);     // fine cnt / start / cursor / big list
+  b += 2 * align_up(((size_t)L.nb1 + 1) * 4, 256) + 256; // c_start, tp, big count
+  b += align_up(n * kb, 256);                            // level-1 output
+  if (query) {
+    b += align_up(n * kb, 256);                          // level-2 output
+    b += 2 * align_up(n * 2, 256);                       // pmap1, pmap2
+    b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
+    b += align_up(L.max_tiles2 * (2 * kSub + 1) * 4, 256);  // meta2
+    b += align_up(n * 4, 256);                           // bin-ordered multiplicities
+  } else {
+    b += align_up((size_t)num_sms() * (1u << L.s) * 4, 256);  // big-bin scratch
+  }
+  return b + 4096;
 }
 
-struct PartitionOut {
-  void* part;
+struct PartOut {
+  const void* grouped;  // keys grouped by fine bin at fine_start positions
+  void* out1;           // level-1 buffer (n keys of workspace)
   uint32_t* M;
-  uint32_t* bin_start;
+  uint32_t* fine_start;
+  uint32_t* c_start;
+  uint32_t* tp;
   uint32_t* big_list;
   uint32_t* big_count;
-  uint16_t* pmap;
+  uint16_t* pmap1;
+  uint16_t* pmap2;
+  uint32_t* meta1;
+  uint32_t* meta2;
 };
 
+// Passes A + P1 (+ P2).  Build mode with two levels writes the fine-grouped
+// keys into `final_out`; otherwise they stay in workspace buffers.
 template <typename K>
-static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap,
-                         bool want_pmap, Workspace& ws, cudaStream_t st, PartitionOut* po) {
-  uint32_t* M = ws.take<uint32_t>((size_t)L.grid * L.nbins);
-  uint32_t* totals = ws.take<uint32_t>(L.nbins);
-  po->M = M;
-  po->bin_start = ws.take<uint32_t>(L.nbins + 1);
-  po->big_list = ws.take<uint32_t>(L.nbins);
+static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap, bool query,
+                         K* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
+  uint32_t* fine_cnt = ws.take<uint32_t>(L.nfine + 1);
+  po->fine_start = ws.take<uint32_t>(L.nfine + 1);
+  uint32_t* fine_cursor = ws.take<uint32_t>(L.nfine + 1);
+  po->big_list = ws.take<uint32_t>(L.nfine + 1);
+  po->c_start = ws.take<uint32_t>(L.nb1 + 1);
+  po->tp = ws.take<uint32_t>(L.nb1 + 1);
   po->big_count = ws.take<uint32_t>(64);
-  K* part = ws.take<K>(n);
-  po->part = part;
-  po->pmap = want_pmap ? ws.take<uint16_t>(n) : nullptr;
-  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small (%zu < %zu)", ws.cap, ws.used);
-  size_t smA = (size_t)L.nbins * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_bin_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
-  HG_LAUNCH("hg_bin_count", k_bin_count<K>, L.grid, kBT, smA, st, keys, n, hp, L.s, L.nbins, L.chunk, M);
-  HG_LAUNCH("hg_bin_colscan", k_bin_colscan, (L.nbins + 255) / 256, 256, 0, st, M, L.grid, L.nbins, totals);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_bin_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
-  HG_LAUNCH("hg_bin_starts", k_bin_starts, 1, kBT, smA, st, totals, L.nbins, cap, po->bin_start, po->big_list,
-            po->big_count);
-  size_t smB = partition_smem(L, sizeof(K) * 8);
-  if (want_pmap) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_partition<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB));
-    HG_LAUNCH("hg_partition_slot", (k_partition<K, true>), L.grid, kBT, smB, st, keys, n, hp, L.s, L.nbins, L.chunk, M,
-              po->bin_start, part, po->pmap);
+  po->M = ws.take<uint32_t>((size_t)L.grid * L.nb1);
+  K* out1 = ws.take<K>(n);
+  K* out2 = nullptr;
+  po->out1 = out1;
+  po->pmap1 = po->pmap2 = nullptr;
+  po->meta1 = po->meta2 = nullptr;
+  if (query) {
+    out2 = L.two_level ? ws.take<K>(n) : nullptr;
+    po->pmap1 = ws.take<uint16_t>(n);
+    po->pmap2 = L.two_level ? ws.take<uint16_t>(n) : nullptr;
+    po->meta1 = ws.take<uint32_t>(L.ntiles1 * (L.nb1 + 1));
+    po->meta2 = L.two_level ? ws.take<uint32_t>(L.max_tiles2 * (2 * kSub + 1)) : nullptr;
   } else {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_partition<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB));
-    HG_LAUNCH("hg_partition", (k_partition<K, false>), L.grid, kBT, smB, st, keys, n, hp, L.s, L.nbins, L.chunk, M,
-              po->bin_start, part, po->pmap);
+    out2 = final_out;
+  }
+  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small (%zu < %zu)", ws.cap, ws.used);
+  HG_CHECK_CUDA(cudaMemsetAsync(fine_cnt, 0, 4 * (size_t)L.nfine, st));
+  const size_t smA = (size_t)L.nfine * 4;
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+  HG_LAUNCH("hg_hist", k_hist<K>, L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk, po->M,
+            fine_cnt);
+  HG_LAUNCH("hg_colscan", k_colscan, (L.nb1 + 127) / 128, 128, 0, st, po->M, L.grid, L.nb1);
+  const size_t smS = ((size_t)L.nfine + L.nb1 + 1) * 4;
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smS));
+  HG_LAUNCH("hg_starts", k_starts, 1, 1024, smS, st, fine_cnt, L.nfine, L.group, L.nb1, L.tile, cap, po->fine_start,
+            po->c_start, po->tp, fine_cursor, po->big_list, po->big_count);
+  const size_t smP = part_smem(sizeof(K) * 8);
+  if (query) {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_LAUNCH("hg_part1_q", (k_part1<K, true>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
+              po->M, po->c_start, out1, po->pmap1, po->meta1);
+  } else {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_LAUNCH("hg_part1", (k_part1<K, false>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
+              po->M, po->c_start, out1, nullptr, nullptr);
+  }
+  if (L.two_level) {
+    if (query) {
+      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_LAUNCH("hg_part2_q", (k_part2<K, true>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+                fine_cursor, out2, po->pmap2, po->meta2);
+    } else {
+      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_LAUNCH("hg_part2", (k_part2<K, false>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+                fine_cursor, out2, nullptr, nullptr);
+    }
+    po->grouped = out2;
+  } else {
+    po->grouped = out1;
   }
   return HG_OK;
 }
@@ -716,17 +919,20 @@ static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const 
 template <typename K>
 int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
                  K* edges, Workspace& ws, cudaStream_t st) {
-  const uint32_t cap = BuildShape<K>::kCap;
-  PartitionOut po{};
-  int rc = run_partition<K>(keys, n, hp, L, cap, false, ws, st, &po);
+  PartOut po{};
+  int rc = run_partition<K>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
   if (rc) return rc;
   uint32_t* scratch = ws.take<uint32_t>((size_t)num_sms() * (1u << L.s));
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
-  size_t smC = build_smem(L, sizeof(K) * 8);
+  const size_t smC = local_smem(L.s, sizeof(K) * 8);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
-  HG_LAUNCH("hg_local_build", k_local_build<K>, L.nbins, kBT, smC, st, (const K*)po.part, po.bin_start, L.nbins, hp,
-            L.s, v, offsets, edges);
-  HG_LAUNCH("hg_local_build_big", k_local_build_big<K>, num_sms(), kBT, 0, st, (const K*)po.part, po.bin_start,
+  const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
+  HG_LAUNCH("hg_local_build", k_local_build<K>, L.nfine, kT, smC, st, grouped, po.fine_start, L.nfine, hp, L.s, v,
+            offsets, edges);
+  // oversized fine bins: with two levels their keys sit in edges (in place), so
+  // they are copied to the free level-1 buffer first
+  const int copy = L.two_level ? 1 : 0;
+  HG_LAUNCH("hg_local_build_big", k_local_build_big<K>, num_sms(), 1024, 0, st, (K*)po.out1, copy, po.fine_start,
             po.big_list, po.big_count, hp, L.s, v, scratch, offsets, edges);
   return HG_OK;
 }
@@ -734,20 +940,27 @@ int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, co
 template <typename K>
 int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
                  uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
-  PartitionOut po{};
-  int rc = run_partition<K>(queries, q, hp, L, 0xFFFFFFFFu, true, ws, st, &po);
+  PartOut po{};
+  int rc = run_partition<K>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
   if (rc) return rc;
   uint32_t* mult_bo = ws.take<uint32_t>(q);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
-  const uint32_t cap = caps_for(sizeof(K) * 8, kProbeCap);
-  size_t smC = probe_smem(L, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
-  HG_LAUNCH("hg_local_probe", k_local_probe<K>, L.nbins, kBT, smC, st, t_off, t_edges, (const K*)po.part, po.bin_start,
-            hp, L.s, v, cap, mult_bo, reinterpret_cast<unsigned long long*>(agg));
-  size_t smR = partition_smem(L, 32);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpartition<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
-  HG_LAUNCH("hg_unpartition", k_unpartition<K>, L.grid, kBT, smR, st, queries, q, hp, L.s, L.nbins, L.chunk, po.M,
-            po.bin_start, mult_bo, po.pmap, mult);
+  const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
+  HG_LAUNCH("hg_local_probe", k_local_probe<K>, L.nfine, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
+            po.fine_start, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  const size_t smR = unpart_smem();
+  uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
+  if (L.two_level) {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, mult_bo, level1_vals, po.pmap2, po.meta2, L.nb1, L.tile,
+              q, L.chunk, po.M, po.c_start, po.tp);
+  } else {
+    level1_vals = mult_bo;
+  }
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+  HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.nb1, L.tile, q,
+            L.chunk, po.M, po.c_start, po.tp);
   return HG_OK;
 }
 

@@ -1,0 +1,31 @@
+// hg_binned.cuh -- interface of the binned build/query path (hg_binned.cu).
+#pragma once
+#include "hg_common.cuh"
+
+namespace hg {
+
+struct BinLayout {
+  int s;               // log2 buckets per fine bin
+  uint32_t nfine;      // F
+  bool two_level;
+  uint32_t nb1;        // level-1 bins (F when one level)
+  int bits1;           // ballot bits for level 1
+  int shift1;          // level-1 bin = bucket >> shift1
+  uint32_t group;      // fine bins per level-1 bin (1 or 128)
+  uint32_t grid;       // CTAs of A / P1 / R1 (one chunk each)
+  uint64_t chunk;      // keys per chunk (multiple of the tile)
+  uint32_t tile;
+  uint64_t ntiles1;
+  uint64_t max_tiles2;
+};
+
+bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L);
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query);
+template <typename K>
+int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
+                 K* edges, Workspace& ws, cudaStream_t st);
+template <typename K>
+int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st);
+
+}  // namespace hg

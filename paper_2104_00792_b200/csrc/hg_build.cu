@@ -9,7 +9,7 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "hg_common.cuh"
+#include "hg_binned.cuh"
 
 namespace hg {
 
@@ -263,23 +263,6 @@ int intersect_impl(const uint32_t* off_a, const K* edges_a, const K* edges_b, co
             n_b, hp, mult, reinterpret_cast<unsigned long long*>(agg));
   return HG_OK;
 }
-
-// v2 binned path (hg_binned.cu)
-struct BinLayout {
-  int s;
-  uint32_t nbins;
-  uint32_t tile;
-  uint32_t grid;
-  uint64_t chunk;
-};
-bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L);
-size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query);
-template <typename K>
-int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
-                 K* edges, Workspace& ws, cudaStream_t st);
-template <typename K>
-int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st);
 
 constexpr uint64_t kBinnedMin = 1ull << 16;  // below this the 3-kernel direct path wins
 
