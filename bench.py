@@ -59,68 +59,85 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clock + throttle reasons during the timed region."""
+    """NVML sampling (in-process thread) of SM clock + throttle reasons during
+    the timed region; falls back to an nvidia-smi subprocess."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.05):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []
+        self.stop_flag = threading.Event()
+        self.thread = None
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop_flag.is_set():
+                    try:
+                        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                        self.samples.append((mhz, reasons, util))
+                    except Exception as e:  # noqa: BLE001
+                        self.err = str(e)
+                    self.stop_flag.wait(self.period)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) != 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:]):
-                if val.lower().startswith("active"):
+        self.stop_flag.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"]}
+        loaded = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = set()
+        for _, r, _ in loaded:
+            for name, bit in self.REASONS.items():
+                if r & bit:
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(s[0] for s in loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples), "samples_under_load": len(loaded)}
 
 
 # --------------------------------------------------------------------------- roofline bookkeeping
 
 
 def algorithmic_bytes(name: str, n: int, q: int, v: int, w: int = 4) -> float:
-    """Per-launch algorithmic bytes: the kernel's minimal
-    HBM I/O, not counting scratch."""
+    """Per-launch algorithmic bytes of each kernel (Kernels): the
+    HBM bytes its job must move at minimum -- inputs read once, outputs
+    written once; scratch such as counters is not counted."""
     table = {
-        "hg_count": w * n,                      # read keys
-        "hg_scan": 4 * v + 4 * (v + 1),         # read counts, write offsets
-        "hg_place": 2 * w * n,                  # read keys, write edges
-        "hg_place_pos": 2 * w * q + 4 * q,      # + positions
-        "hg_intersect": 2 * w * q + 4 * q + 4 * q + w * n + 4 * (v + 1),  # q edges+pos, mult, table
+        # direct (Alg. 1) path
+        "hg_count": w * n,
+        "hg_scan": 4 * v + 4 * (v + 1),
+        "hg_place": 2 * w * n,
+        "hg_place_pos": 2 * w * q + 4 * q,
+        "hg_intersect": 2 * w * q + 4 * q + 4 * q + w * n + 4 * (v + 1),
+        # binned path, build side (n keys)
+        "hg_hist": w * n,
+        "hg_part1": 2 * w * n,
+        "hg_part2": 2 * w * n,
+        "hg_local_build": 2 * w * n + 4 * (v + 1),
+        # binned path, query side (q queries against n table keys)
+        "hg_part1_q": 2 * w * q + 2 * q,
+        "hg_part2_q": 2 * w * q + 2 * q,
+        "hg_local_probe": w * q + w * n + 4 * (v + 1) + 4 * q,
+        "hg_unpart2": 4 * q + 2 * q + 4 * q,
+        "hg_unpart1": 4 * q + 2 * q + 4 * q,
     }
     return float(table.get(name, 0))
 

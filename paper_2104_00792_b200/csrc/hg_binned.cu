@@ -83,9 +83,12 @@ bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLa
   return true;
 }
 
-template <typename K>
-__device__ __forceinline__ uint32_t fine_of(K key, const HashParams& hp, int s) {
-  return bucket_of(key, hp) >> s;
+template <typename H>
+using KeyOf = typename H::Key;
+
+template <typename H>
+__device__ __forceinline__ uint32_t fine_of(typename H::Key key, const HashParams& hp, int s) {
+  return H::bucket(key, hp) >> s;
 }
 
 // --------------------------------------------------------------------------- block helpers
@@ -238,10 +241,11 @@ __device__ __forceinline__ bool load_tile(const K* __restrict__ src, uint32_t m,
 
 // --------------------------------------------------------------------------- pass A
 
-template <typename K>
+template <typename H>
 __global__ void __launch_bounds__(kT)
-k_hist(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nfine, uint32_t group, uint32_t nb1,
+k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nfine, uint32_t group, uint32_t nb1,
        uint64_t chunk, uint32_t* __restrict__ M, uint32_t* __restrict__ fine_cnt) {
+  using K = typename H::Key;
   extern __shared__ uint32_t s_h[];
   for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
@@ -257,22 +261,22 @@ k_hist(const K* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nf
       for (int u = 0; u < 4; u++) q[u] = __ldcs(p + i + u * blockDim.x);
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        atomicAdd(s_h + fine_of((K)q[u].x, hp, s), 1u);
-        atomicAdd(s_h + fine_of((K)q[u].y, hp, s), 1u);
-        atomicAdd(s_h + fine_of((K)q[u].z, hp, s), 1u);
-        atomicAdd(s_h + fine_of((K)q[u].w, hp, s), 1u);
+        atomicAdd(s_h + fine_of<H>((K)q[u].x, hp, s), 1u);
+        atomicAdd(s_h + fine_of<H>((K)q[u].y, hp, s), 1u);
+        atomicAdd(s_h + fine_of<H>((K)q[u].z, hp, s), 1u);
+        atomicAdd(s_h + fine_of<H>((K)q[u].w, hp, s), 1u);
       }
     }
     for (; i < nv; i += blockDim.x) {
       uint4 q = __ldcs(p + i);
-      atomicAdd(s_h + fine_of((K)q.x, hp, s), 1u);
-      atomicAdd(s_h + fine_of((K)q.y, hp, s), 1u);
-      atomicAdd(s_h + fine_of((K)q.z, hp, s), 1u);
-      atomicAdd(s_h + fine_of((K)q.w, hp, s), 1u);
+      atomicAdd(s_h + fine_of<H>((K)q.x, hp, s), 1u);
+      atomicAdd(s_h + fine_of<H>((K)q.y, hp, s), 1u);
+      atomicAdd(s_h + fine_of<H>((K)q.z, hp, s), 1u);
+      atomicAdd(s_h + fine_of<H>((K)q.w, hp, s), 1u);
     }
-    for (uint64_t j = lo + nv * 4 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of(keys[j], hp, s), 1u);
+    for (uint64_t j = lo + nv * 4 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
   } else {
-    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of(keys[j], hp, s), 1u);
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
   }
   __syncthreads();
   uint32_t* row = M + (uint64_t)blockIdx.x * nb1;
@@ -354,9 +358,10 @@ struct PartSmem {
 // stays in registers); a per-bin prefix over warps then gives every key its
 // staged slot.  Afterwards s.toff holds the tile offsets.  pmap (optional)
 // receives each key's staged position, indexed by its tile element.
-template <typename K, int KPT>
+template <typename K, int KPT, bool kFull>
 __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT], const uint32_t (&bp)[KPT / 4],
-                                               uint32_t m, bool vec, uint32_t nb, uint16_t* __restrict__ pmap) {
+                                               uint32_t m, uint32_t nb, uint16_t* __restrict__ pmap) {
+  constexpr bool vec = kFull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t b = lane; b < nb; b += 32) s.wcnt[warp][b] = 0;
   __syncwarp();
@@ -365,7 +370,7 @@ __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT
   for (int k = 0; k < KPT; k++) {
     const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
     uint32_t r = 0;
-    if (tile_elem<K>(k, vec) < m) r = atomicAdd(&s.wcnt[warp][b], 1u);
+    if (kFull || tile_elem<K>(k, vec) < m) r = atomicAdd(&s.wcnt[warp][b], 1u);
     if (k & 1) rk[k >> 1] |= r << 16; else rk[k >> 1] = r;
   }
   __syncthreads();
@@ -391,7 +396,7 @@ __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT
 #pragma unroll
   for (int k = 0; k < KPT; k++) {
     const uint32_t e = tile_elem<K>(k, vec);
-    if (e < m) {
+    if (kFull || e < m) {
       const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
       const uint32_t slot = s.wcnt[warp][b] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
       s.staged[slot] = kv[k];
@@ -415,11 +420,12 @@ __device__ __forceinline__ void write_runs(const PartSmem<K>& s, uint32_t nb, K*
 // Level 1: CTA chunk tiles, bin = bucket >> shift1, deterministic bases
 // (column-scanned per-CTA counts).  Query mode also records the u16 staged
 // position of every key (pmap) and each tile's offsets (meta, nb+1 words).
-template <typename K, bool kQuery>
+template <typename H, bool kQuery>
 __global__ void __launch_bounds__(kT, 2)
-k_part1(const K* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int bits1, uint32_t nb1, uint64_t chunk,
-        const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, K* __restrict__ out,
+k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int bits1, uint32_t nb1, uint64_t chunk,
+        const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, KeyOf<H>* __restrict__ out,
         uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
+  using K = typename H::Key;
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -435,12 +441,13 @@ k_part1(const K* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int b
     uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
-      const uint32_t b = (uint32_t)(bucket_of(kv[k], hp) >> shift1);
+      const uint32_t b = (uint32_t)(H::bucket(kv[k], hp) >> shift1);
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= (b & 0xFFu) << ((k & 3) * 8);
     }
     __syncthreads();  // previous tile fully written out
-    rank_and_stage<K, KPT>(s, kv, bp, m, vec, nb1, kQuery ? pmap + t0 : nullptr);
+    if (vec) rank_and_stage<K, KPT, true>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
+    else rank_and_stage<K, KPT, false>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
     write_runs<K>(s, nb1, out);
     if (kQuery)
       for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) meta[(t0 / TS::kTile) * (nb1 + 1) + i] = s.toff[i];
@@ -452,11 +459,12 @@ k_part1(const K* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int b
 // Level 2: tiles of each level-1 bin, sub-bin = fine & 127, space claimed per
 // (tile, fine bin) from the fine cursors.  Query mode records pmap (indexed in
 // level-1 order) and meta = [128 claims | 129 tile offsets] per tile.
-template <typename K, bool kQuery>
+template <typename H, bool kQuery>
 __global__ void __launch_bounds__(kT, 2)
-k_part2(const K* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
-        const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, K* __restrict__ out,
+k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
+        const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, KeyOf<H>* __restrict__ out,
         uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
+  using K = typename H::Key;
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -478,12 +486,13 @@ k_part2(const K* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const 
     uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
-      const uint32_t b = (uint32_t)(bucket_of(kv[k], hp) >> s_log) & (kSub - 1);
+      const uint32_t b = (uint32_t)(H::bucket(kv[k], hp) >> s_log) & (kSub - 1);
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= b << ((k & 3) * 8);
     }
     __syncthreads();
-    rank_and_stage<K, KPT>(s, kv, bp, m, vec, kSub, kQuery ? pmap + t0 : nullptr);
+    if (vec) rank_and_stage<K, KPT, true>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
+    else rank_and_stage<K, KPT, false>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
     if (threadIdx.x < kSub) {
       const uint32_t cnt = s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
       s.dst[threadIdx.x] = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
@@ -581,7 +590,19 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) out[t0 + i] = staged[pmap[t0 + i]];
+    {
+      uint32_t pm[VPT];  // position maps first (all loads in flight), then the smem gathers
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t i = k * kT + threadIdx.x;
+        pm[k] = i < m ? pmap[t0 + i] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t i = k * kT + threadIdx.x;
+        if (i < m) out[t0 + i] = staged[pm[k]];
+      }
+    }
     if (kLevel == 1) {
       __syncthreads();
       if (threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
@@ -594,10 +615,11 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
 // One CTA per fine bin (two CTAs per SM): keys in registers, packed-u16 smem
 // counters, scan, place, then offsets and edges leave as coalesced streams.
 // `src` may alias `edges` (each CTA reads its whole range before writing it).
-template <typename K>
+template <typename H>
 __global__ void __launch_bounds__(kT, 2)
-k_local_build(const K* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s, uint64_t v,
-              uint32_t* __restrict__ offsets, K* edges) {
+k_local_build(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s, uint64_t v,
+              uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
+  using K = typename H::Key;
   constexpr int KPT = LocalShape<K>::kKPT;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
@@ -621,7 +643,7 @@ k_local_build(const K* src, const uint32_t* __restrict__ fine_start, uint32_t nf
 #pragma unroll
   for (int k = 0; k < KPT; k++)
     if (k * kT + threadIdx.x < cnt) {
-      const uint32_t l = bucket_of(kv[k], hp) - (uint32_t)first;
+      const uint32_t l = H::bucket(kv[k], hp) - (uint32_t)first;
       atomicAdd(c16 + (l >> 1), 1u << ((l & 1) * 16));
     }
   __syncthreads();
@@ -631,7 +653,7 @@ k_local_build(const K* src, const uint32_t* __restrict__ fine_start, uint32_t nf
 #pragma unroll
   for (int k = 0; k < KPT; k++)
     if (k * kT + threadIdx.x < cnt) {
-      const uint32_t l = bucket_of(kv[k], hp) - (uint32_t)first;
+      const uint32_t l = H::bucket(kv[k], hp) - (uint32_t)first;
       const uint32_t sh = (l & 1) * 16;
       const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sh);
       staged[(old >> sh) & 0xFFFFu] = kv[k];
@@ -643,11 +665,12 @@ k_local_build(const K* src, const uint32_t* __restrict__ fine_start, uint32_t nf
 // Fine bins above the smem capacity: global-memory counters (one 2^s scratch
 // per CTA).  When `copy` is set the bin is first copied from `edges` into
 // `src` (same offsets) so placement can overwrite edges.
-template <typename K>
+template <typename H>
 __global__ void __launch_bounds__(1024)
-k_local_build_big(K* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
+k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
                   const uint32_t* __restrict__ big_count, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ scratch,
-                  uint32_t* __restrict__ offsets, K* edges) {
+                  uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
+  using K = typename H::Key;
   const uint32_t S = 1u << s;
   uint32_t* cnt = scratch + (uint64_t)blockIdx.x * S;
   __shared__ uint32_t s_w[32];
@@ -660,7 +683,7 @@ k_local_build_big(K* src, int copy, const uint32_t* __restrict__ fine_start, con
       for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) src[j] = edges[j];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(cnt + (bucket_of(src[j], hp) - (uint32_t)first), 1u);
+    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(cnt + (H::bucket(src[j], hp) - (uint32_t)first), 1u);
     __syncthreads();
     const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
     const uint32_t a0 = threadIdx.x * per, a1 = min(a0 + per, nb);
@@ -693,7 +716,7 @@ k_local_build_big(K* src, int copy, const uint32_t* __restrict__ fine_start, con
     __syncthreads();
     for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
       const K key = src[j];
-      edges[atomicAdd(cnt + (bucket_of(key, hp) - (uint32_t)first), 1u)] = key;
+      edges[atomicAdd(cnt + (H::bucket(key, hp) - (uint32_t)first), 1u)] = key;
     }
     __syncthreads();
   }
@@ -720,11 +743,12 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
 // (count of equal keys in the bucket; comparisons += bucket
 // degree, query.py:153-155) and write counts in partitioned order.  Slices
 // above the smem capacity are probed in global memory.
-template <typename K>
+template <typename H>
 __global__ void __launch_bounds__(kT, 2)
-k_local_probe(const uint32_t* __restrict__ t_off, const K* __restrict__ t_edges, const K* __restrict__ qpart,
+k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t_edges, const KeyOf<H>* __restrict__ qpart,
               const uint32_t* __restrict__ q_start, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ mult_bo,
               unsigned long long* __restrict__ agg) {
+  using K = typename H::Key;
   constexpr int QPT = 16;
   constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -781,7 +805,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const K* __restrict__ t_edges,
       const uint32_t j = q0 + k * kT + threadIdx.x;
       if (j < qhi) {
         const K q = qv[k];
-        const uint32_t h = bucket_of(q, hp);
+        const uint32_t h = H::bucket(q, hp);
         uint32_t a, e, c = 0;
         if (in_smem) {
           const uint32_t l = h - (uint32_t)first;
@@ -853,9 +877,10 @@ struct PartOut {
 
 // Passes A + P1 (+ P2).  Build mode with two levels writes the fine-grouped
 // keys into `final_out`; otherwise they stay in workspace buffers.
-template <typename K>
-static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap, bool query,
-                         K* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
+template <typename H>
+static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap, bool query,
+                         KeyOf<H>* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
+  using K = KeyOf<H>;
   uint32_t* fine_cnt = ws.take<uint32_t>(L.nfine + 1);
   po->fine_start = ws.take<uint32_t>(L.nfine + 1);
   uint32_t* fine_cursor = ws.take<uint32_t>(L.nfine + 1);
@@ -881,8 +906,8 @@ static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const 
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small (%zu < %zu)", ws.cap, ws.used);
   HG_CHECK_CUDA(cudaMemsetAsync(fine_cnt, 0, 4 * (size_t)L.nfine, st));
   const size_t smA = (size_t)L.nfine * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
-  HG_LAUNCH("hg_hist", k_hist<K>, L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk, po->M,
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+  HG_LAUNCH("hg_hist", k_hist<H>, L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk, po->M,
             fine_cnt);
   HG_LAUNCH("hg_colscan", k_colscan, (L.nb1 + 127) / 128, 128, 0, st, po->M, L.grid, L.nb1);
   const size_t smS = ((size_t)L.nfine + L.nb1 + 1) * 4;
@@ -891,22 +916,22 @@ static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const 
             po->c_start, po->tp, fine_cursor, po->big_list, po->big_count);
   const size_t smP = part_smem(sizeof(K) * 8);
   if (query) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-    HG_LAUNCH("hg_part1_q", (k_part1<K, true>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_LAUNCH("hg_part1_q", (k_part1<H, true>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
               po->M, po->c_start, out1, po->pmap1, po->meta1);
   } else {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-    HG_LAUNCH("hg_part1", (k_part1<K, false>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_LAUNCH("hg_part1", (k_part1<H, false>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
               po->M, po->c_start, out1, nullptr, nullptr);
   }
   if (L.two_level) {
     if (query) {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2_q", (k_part2<K, true>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_LAUNCH("hg_part2_q", (k_part2<H, true>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
                 fine_cursor, out2, po->pmap2, po->meta2);
     } else {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2", (k_part2<K, false>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_LAUNCH("hg_part2", (k_part2<H, false>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
                 fine_cursor, out2, nullptr, nullptr);
     }
     po->grouped = out2;
@@ -916,38 +941,40 @@ static int run_partition(const K* keys, uint64_t n, const HashParams& hp, const 
   return HG_OK;
 }
 
-template <typename K>
-int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
-                 K* edges, Workspace& ws, cudaStream_t st) {
+template <typename H>
+static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
+                 KeyOf<H>* edges, Workspace& ws, cudaStream_t st) {
+  using K = KeyOf<H>;
   PartOut po{};
-  int rc = run_partition<K>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
+  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
   if (rc) return rc;
   uint32_t* scratch = ws.take<uint32_t>((size_t)num_sms() * (1u << L.s));
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const size_t smC = local_smem(L.s, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
   const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
-  HG_LAUNCH("hg_local_build", k_local_build<K>, L.nfine, kT, smC, st, grouped, po.fine_start, L.nfine, hp, L.s, v,
+  HG_LAUNCH("hg_local_build", k_local_build<H>, L.nfine, kT, smC, st, grouped, po.fine_start, L.nfine, hp, L.s, v,
             offsets, edges);
   // oversized fine bins: with two levels their keys sit in edges (in place), so
   // they are copied to the free level-1 buffer first
   const int copy = L.two_level ? 1 : 0;
-  HG_LAUNCH("hg_local_build_big", k_local_build_big<K>, num_sms(), 1024, 0, st, (K*)po.out1, copy, po.fine_start,
+  HG_LAUNCH("hg_local_build_big", k_local_build_big<H>, num_sms(), 1024, 0, st, (K*)po.out1, copy, po.fine_start,
             po.big_list, po.big_count, hp, L.s, v, scratch, offsets, edges);
   return HG_OK;
 }
 
-template <typename K>
-int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
+template <typename H>
+static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyOf<H>* queries, uint64_t q, const HashParams& hp,
                  uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
+  using K = KeyOf<H>;
   PartOut po{};
-  int rc = run_partition<K>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
+  int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
   if (rc) return rc;
   uint32_t* mult_bo = ws.take<uint32_t>(q);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
-  HG_LAUNCH("hg_local_probe", k_local_probe<K>, L.nfine, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
+  HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
             po.fine_start, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
   const size_t smR = unpart_smem();
   uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
@@ -962,6 +989,41 @@ int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint
   HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.nb1, L.tile, q,
             L.chunk, po.M, po.c_start, po.tp);
   return HG_OK;
+}
+
+template <typename K>
+int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
+                 K* edges, Workspace& ws, cudaStream_t st) {
+  switch (hp.mode) {
+    case kMask:
+      return build_impl<Hasher<K, kMask>>(keys, n, hp, v, L, offsets, edges, ws, st);
+    case kNone:
+      if constexpr (sizeof(K) == 4) return build_impl<Hasher<K, kNone>>(keys, n, hp, v, L, offsets, edges, ws, st);
+      [[fallthrough]];
+    case kFastmod:
+      if constexpr (sizeof(K) == 4) return build_impl<Hasher<K, kFastmod>>(keys, n, hp, v, L, offsets, edges, ws, st);
+      [[fallthrough]];
+    default:
+      return build_impl<Hasher<K, kGeneric64>>(keys, n, hp, v, L, offsets, edges, ws, st);
+  }
+}
+
+template <typename K>
+int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
+  switch (hp.mode) {
+    case kMask:
+      return query_impl<Hasher<K, kMask>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+    case kNone:
+      if constexpr (sizeof(K) == 4) return query_impl<Hasher<K, kNone>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+      [[fallthrough]];
+    case kFastmod:
+      if constexpr (sizeof(K) == 4)
+        return query_impl<Hasher<K, kFastmod>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+      [[fallthrough]];
+    default:
+      return query_impl<Hasher<K, kGeneric64>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+  }
 }
 
 template int binned_build<uint32_t>(const uint32_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,

@@ -122,6 +122,25 @@ __device__ __forceinline__ uint64_t hash_mod(K key, const HashParams& hp) {
   }
 }
 
+// Compile-time specialised hasher: MODE fixes the reduction (kMask, kFastmod,
+// kNone, kGeneric64) so the hot loops carry no per-key dispatch.
+template <typename K, int MODE>
+struct Hasher {
+  using Key = K;
+  static __device__ __forceinline__ uint32_t bucket(K key, const HashParams& hp) {
+    const uint64_t x = mix_key(key, hp);
+    if constexpr (MODE == kMask) {
+      return (uint32_t)(x & hp.mask);
+    } else if constexpr (MODE == kNone) {
+      return (uint32_t)x;
+    } else if constexpr (MODE == kFastmod && sizeof(K) == 4) {
+      return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
+    } else {
+      return (uint32_t)(x % hp.v);
+    }
+  }
+};
+
 // Bucket id for builds/queries: v <= 2^32 is enforced on the host, so the
 // result fits uint32.
 template <typename K>
