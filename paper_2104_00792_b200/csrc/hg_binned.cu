@@ -130,42 +130,49 @@ __device__ uint32_t block_exscan(uint32_t* a, uint32_t n) {
   return total;
 }
 
-// Same over n packed uint16 counters (two per word); totals stay < 65536.
+// Exclusive scan of nvals packed uint16 counters (two per word) in smem, in
+// place; totals stay < 65536.  Warp w owns a contiguous segment of words and
+// walks it in 32-word rows (lane = word within row: no bank conflicts).
 __device__ void block_exscan_u16(uint32_t* w16, uint32_t nvals) {
   __shared__ uint32_t s_w[32];
   const uint32_t nwords = (nvals + 1) / 2;
-  const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, nwords);
-  uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; i++) {
-    uint32_t x = w16[i];
-    sum += (x & 0xFFFFu) + (x >> 16);
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t inc = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
+  const uint32_t seg = ((nwords + nw - 1) / nw + 31) & ~31u;
+  const uint32_t w0 = warp * seg, w1 = min(w0 + seg, nwords);
+  uint32_t part = 0;
+  for (uint32_t i = w0 + lane; i < w1; i += 32) {
+    const uint32_t x = w16[i];
+    part += (x & 0xFFFFu) + (x >> 16);
   }
-  if (lane == 31) s_w[warp] = inc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) s_w[warp] = part;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = lane < nw ? s_w[lane] : 0u;
+    uint32_t x = lane < nw ? s_w[lane] : 0u;
+    uint32_t inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    if (lane < nw) s_w[lane] = w;
+    if (lane < nw) s_w[lane] = inc - x;  // exclusive warp bases
   }
   __syncthreads();
-  uint32_t run = (warp ? s_w[warp - 1] : 0u) + inc - sum;
-  for (uint32_t i = lo; i < hi; i++) {
-    uint32_t x = w16[i];
-    uint32_t a = run, b = run + (x & 0xFFFFu);
-    w16[i] = (a & 0xFFFFu) | (b << 16);
-    run = b + (x >> 16);
+  uint32_t carry = s_w[warp];
+  for (uint32_t r = w0; r < w1; r += 32) {
+    const uint32_t i = r + lane;
+    const uint32_t x = i < w1 ? w16[i] : 0u;
+    const uint32_t sx = (x & 0xFFFFu) + (x >> 16);
+    uint32_t inc = sx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t pre = carry + inc - sx;
+    if (i < w1) w16[i] = (pre & 0xFFFFu) | ((pre + (x & 0xFFFFu)) << 16);
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
   __syncthreads();
 }
@@ -346,11 +353,15 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
 
 template <typename K>
 struct PartSmem {
+  K raw[TileShape<K>::kTile + 16 / sizeof(K)];  // TMA landing buffer (next tile)
   K staged[TileShape<K>::kTile];
+  uint8_t bin_at[TileShape<K>::kTile];  // bin of each staged slot
   uint32_t wcnt[kW][kSub];  // per-warp counts -> per-warp slot bases
   uint32_t toff[kSub + 1];  // tile offsets per bin
   uint32_t dst[kSub];       // global write base per bin
+  uint32_t delta[kSub];     // dst - toff: global index of staged slot j is delta[bin] + j
   uint32_t tp[kSub + 1];    // level-2 tile prefix (P2 only)
+  alignas(8) uint64_t bar;  // TMA completion barrier
 };
 
 // Rank a register tile by bin and stage it grouped by bin in smem.  Each key
@@ -400,20 +411,21 @@ __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT
       const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
       const uint32_t slot = s.wcnt[warp][b] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
       s.staged[slot] = kv[k];
+      s.bin_at[slot] = (uint8_t)b;
       if (pmap) pmap[e] = (uint16_t)slot;
     }
   }
   __syncthreads();
 }
 
-// Copy each bin's staged run to out[dst[b] + position in run]: warp per bin.
-template <typename K>
-__device__ __forceinline__ void write_runs(const PartSmem<K>& s, uint32_t nb, K* __restrict__ out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t b = warp; b < nb; b += kW) {
-    const uint32_t lo = s.toff[b], hi = s.toff[b + 1];
-    K* d = out + ((int64_t)s.dst[b] - (int64_t)lo);
-    for (uint32_t j = lo + lane; j < hi; j += 32) d[j] = s.staged[j];
+// Write the staged tile: slot j goes to out[delta[bin_at[j]] + j].  Threads
+// walk consecutive slots, so each warp store covers one or two runs.
+template <typename K, int KPT>
+__device__ __forceinline__ void write_out(const PartSmem<K>& s, uint32_t m, K* __restrict__ out) {
+#pragma unroll
+  for (int k = 0; k < KPT; k++) {
+    const uint32_t j = k * kT + threadIdx.x;
+    if (j < m) out[s.delta[s.bin_at[j]] + j] = s.staged[j];
   }
 }
 
@@ -428,16 +440,41 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
   using K = typename H::Key;
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
-  extern __shared__ __align__(16) unsigned char s_raw[];
+  constexpr int VPL = 16 / sizeof(K);
+  extern __shared__ __align__(128) unsigned char s_raw[];
   PartSmem<K>& s = *reinterpret_cast<PartSmem<K>*>(s_raw);
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;
   const uint64_t hi = min(n, lo + chunk);
   const uint32_t* row = M + (uint64_t)blockIdx.x * nb1;
   if (threadIdx.x < nb1) s.dst[threadIdx.x] = c_start[threadIdx.x] + row[threadIdx.x];
+  // full tiles stream through one TMA buffer: tile i+1 lands while tile i is ranked
+  const bool tma = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&s.bar, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  if (threadIdx.x == 0 && tma && lo + TS::kTile <= hi) tma_load_1d(s.raw, keys + lo, TS::kTile * sizeof(K), &s.bar);
   for (uint64_t t0 = lo; t0 < hi; t0 += TS::kTile) {
     const uint32_t m = (uint32_t)min((uint64_t)TS::kTile, hi - t0);
     K kv[KPT];
-    const bool vec = load_tile<K, KPT>(keys + t0, m, kv);
+    bool vec;
+    if (tma && m == (uint32_t)TS::kTile) {
+      mbar_wait(&s.bar, parity);
+      parity ^= 1;
+      const uint4* r4 = reinterpret_cast<const uint4*>(s.raw);
+#pragma unroll
+      for (int l = 0; l < KPT / VPL; l++) {
+        uint4 q = r4[l * kT + threadIdx.x];
+        const K* qk = reinterpret_cast<const K*>(&q);
+#pragma unroll
+        for (int j = 0; j < VPL; j++) kv[l * VPL + j] = qk[j];
+      }
+      vec = true;
+    } else {
+      vec = load_tile<K, KPT>(keys + t0, m, kv);
+    }
     uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
@@ -445,20 +482,26 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= (b & 0xFFu) << ((k & 3) * 8);
     }
-    __syncthreads();  // previous tile fully written out
+    fence_proxy_async();
+    __syncthreads();  // raw consumed, previous tile fully written out
+    if (threadIdx.x == 0 && tma && t0 + 2 * TS::kTile <= hi)
+      tma_load_1d(s.raw, keys + t0 + TS::kTile, TS::kTile * sizeof(K), &s.bar);
     if (vec) rank_and_stage<K, KPT, true>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
     else rank_and_stage<K, KPT, false>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
-    write_runs<K>(s, nb1, out);
+    if (threadIdx.x < nb1) s.delta[threadIdx.x] = s.dst[threadIdx.x] - s.toff[threadIdx.x];
     if (kQuery)
       for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) meta[(t0 / TS::kTile) * (nb1 + 1) + i] = s.toff[i];
     __syncthreads();
+    write_out<K, KPT>(s, m, out);
     if (threadIdx.x < nb1) s.dst[threadIdx.x] += s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
   }
 }
 
 // Level 2: tiles of each level-1 bin, sub-bin = fine & 127, space claimed per
 // (tile, fine bin) from the fine cursors.  Query mode records pmap (indexed in
-// level-1 order) and meta = [128 claims | 129 tile offsets] per tile.
+// level-1 order) and meta = [128 claims | 129 tile offsets] per tile.  Tiles
+// start anywhere, so the TMA copy starts at the 16-byte boundary below the
+// tile (the input buffer carries 16 bytes of tail padding).
 template <typename H, bool kQuery>
 __global__ void __launch_bounds__(kT, 2)
 k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
@@ -467,22 +510,49 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
   using K = typename H::Key;
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
-  extern __shared__ __align__(16) unsigned char s_raw[];
+  constexpr uint32_t VPL = 16 / sizeof(K);
+  extern __shared__ __align__(128) unsigned char s_raw[];
   PartSmem<K>& s = *reinterpret_cast<PartSmem<K>*>(s_raw);
   for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) s.tp[i] = tp_g[i];
+  if (threadIdx.x == 0) {
+    mbar_init(&s.bar, 1);
+    fence_proxy_async();
+  }
   __syncthreads();
   const uint32_t ntiles = s.tp[nb1];
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  auto locate = [&](uint32_t t, uint32_t& c, uint32_t& t0, uint32_t& m) {
     uint32_t a = 0, z = nb1;  // level-1 bin c: tp[c] <= t < tp[c+1]
     while (z - a > 1) {
       const uint32_t mid = (a + z) >> 1;
       if (s.tp[mid] <= t) a = mid; else z = mid;
     }
-    const uint32_t c = a;
-    const uint32_t t0 = c_start[c] + (t - s.tp[c]) * TS::kTile;
-    const uint32_t m = min((uint32_t)TS::kTile, c_start[c + 1] - t0);
+    c = a;
+    t0 = c_start[c] + (t - s.tp[c]) * TS::kTile;
+    m = min((uint32_t)TS::kTile, c_start[c + 1] - t0);
+  };
+  auto issue = [&](uint32_t t0, uint32_t m) {
+    const uint32_t a0 = t0 & ~(VPL - 1);
+    const uint32_t bytes = ((t0 - a0 + m) * (uint32_t)sizeof(K) + 15) & ~15u;
+    tma_load_1d(s.raw, in + a0, bytes, &s.bar);
+  };
+  uint32_t parity = 0;
+  if (threadIdx.x == 0 && blockIdx.x < ntiles) {
+    uint32_t c, t0, m;
+    locate(blockIdx.x, c, t0, m);
+    issue(t0, m);
+  }
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint32_t c, t0, m;
+    locate(t, c, t0, m);
+    mbar_wait(&s.bar, parity);
+    parity ^= 1;
+    const uint32_t sh = t0 & (VPL - 1);
     K kv[KPT];
-    const bool vec = load_tile<K, KPT>(in + t0, m, kv);
+#pragma unroll
+    for (int k = 0; k < KPT; k++) {
+      const uint32_t e = k * kT + threadIdx.x;
+      kv[k] = e < m ? s.raw[sh + e] : K(0);
+    }
     uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
@@ -490,18 +560,24 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= b << ((k & 3) * 8);
     }
+    fence_proxy_async();
     __syncthreads();
-    if (vec) rank_and_stage<K, KPT, true>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
-    else rank_and_stage<K, KPT, false>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
+    if (threadIdx.x == 0 && t + gridDim.x < ntiles) {
+      uint32_t c2, t02, m2;
+      locate(t + gridDim.x, c2, t02, m2);
+      issue(t02, m2);
+    }
+    rank_and_stage<K, KPT, false>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
     if (threadIdx.x < kSub) {
       const uint32_t cnt = s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
-      s.dst[threadIdx.x] = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
-      if (kQuery) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
+      const uint32_t d = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
+      s.delta[threadIdx.x] = d - s.toff[threadIdx.x];
+      if (kQuery) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = d;
     }
     if (kQuery)
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
     __syncthreads();
-    write_runs<K>(s, kSub, out);
+    write_out<K, KPT>(s, m, out);
   }
 }
 
@@ -612,54 +688,96 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
 
 // --------------------------------------------------------------------------- C: local build
 
-// One CTA per fine bin (two CTAs per SM): keys in registers, packed-u16 smem
-// counters, scan, place, then offsets and edges leave as coalesced streams.
-// `src` may alias `edges` (each CTA reads its whole range before writing it).
+// One CTA per fine bin (two CTAs per SM): the bin's keys arrive with 128-bit
+// loads into registers, packed-u16 smem counters rank them (one atomic per
+// key per pass), and offsets (4 per store) and edges (128-bit stores) leave
+// as aligned coalesced streams.  `src` may alias `edges`: every load of a CTA
+// precedes its first barrier and it only writes inside its own range.
 template <typename H>
 __global__ void __launch_bounds__(kT, 2)
-k_local_build(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s, uint64_t v,
-              uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
+k_local_build(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
+              uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
   using K = typename H::Key;
-  constexpr int KPT = LocalShape<K>::kKPT;
+  constexpr int VPL = 16 / sizeof(K);                       // keys per 16-byte chunk
+  constexpr int NCH = (LocalShape<K>::kKPT + VPL - 1) / VPL + 1;  // chunks per thread
+  constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
   uint32_t* c16 = reinterpret_cast<uint32_t*>(s_raw);  // S/2 words
-  K* staged = reinterpret_cast<K*>(s_raw + (S / 2) * 4);
+  K* staged = reinterpret_cast<K*>(s_raw + (S / 2) * 4);  // kCap + VPL keys, chunk-aligned to global
   const uint32_t f = blockIdx.x;
   const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
   const uint32_t cnt = hi - lo;
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   if (f == nfine - 1 && threadIdx.x == 0) offsets[v] = hi;
-  if (cnt > LocalShape<K>::kCap) return;  // k_local_build_big
-  K kv[KPT];
+  if (cnt > kCap) return;  // k_local_build_big
+  const uint32_t lo_al = lo & ~(uint32_t)(VPL - 1);
+  const uint32_t nch = (hi - lo_al + VPL - 1) / VPL;
+  const uint4* src4 = reinterpret_cast<const uint4*>(src + lo_al);
+  K kv[NCH * VPL];
 #pragma unroll
-  for (int k = 0; k < KPT; k++) {
-    const uint32_t j = k * kT + threadIdx.x;
-    kv[k] = j < cnt ? src[lo + j] : K(0);
+  for (int i = 0; i < NCH; i++) {
+    const uint32_t c = i * kT + threadIdx.x;
+    uint4 q = make_uint4(0, 0, 0, 0);
+    if (c < nch) q = src4[c];
+    const K* qk = reinterpret_cast<const K*>(&q);
+#pragma unroll
+    for (int j = 0; j < VPL; j++) kv[i * VPL + j] = qk[j];
   }
   for (uint32_t i = threadIdx.x; i < (nb + 1) / 2; i += blockDim.x) c16[i] = 0;
   __syncthreads();
+  auto valid = [&](int i, int j) {
+    const uint32_t g = lo_al + (i * kT + threadIdx.x) * VPL + j;
+    return (i * kT + threadIdx.x) < nch && g >= lo && g < hi;
+  };
 #pragma unroll
-  for (int k = 0; k < KPT; k++)
-    if (k * kT + threadIdx.x < cnt) {
-      const uint32_t l = H::bucket(kv[k], hp) - (uint32_t)first;
-      atomicAdd(c16 + (l >> 1), 1u << ((l & 1) * 16));
-    }
+  for (int i = 0; i < NCH; i++)
+#pragma unroll
+    for (int j = 0; j < VPL; j++)
+      if (valid(i, j)) {
+        const uint32_t l = H::bucket(kv[i * VPL + j], hp) - (uint32_t)first;
+        atomicAdd(c16 + (l >> 1), 1u << ((l & 1) * 16));
+      }
   __syncthreads();
   block_exscan_u16(c16, nb);
-  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = lo + get16(c16, i);
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < KPT; k++)
-    if (k * kT + threadIdx.x < cnt) {
-      const uint32_t l = H::bucket(kv[k], hp) - (uint32_t)first;
-      const uint32_t sh = (l & 1) * 16;
-      const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sh);
-      staged[(old >> sh) & 0xFFFFu] = kv[k];
+  // offsets: word pair (2 words = 4 values) per thread -> one 16-byte store
+  for (uint32_t w = threadIdx.x; 4 * w < nb; w += blockDim.x) {
+    const uint32_t a = c16[2 * w], b = (2 * w + 1) * 2 < nb + 1 ? c16[2 * w + 1] : 0u;
+    const uint4 o = make_uint4(lo + (a & 0xFFFFu), lo + (a >> 16), lo + (b & 0xFFFFu), lo + (b >> 16));
+    if (4 * w + 3 < nb) {
+      *reinterpret_cast<uint4*>(offsets + first + 4 * w) = o;
+    } else {
+      const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+      for (uint32_t e = 0; 4 * w + e < nb; e++) offsets[first + 4 * w + e] = ov[e];
     }
+  }
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) edges[lo + j] = staged[j];
+  const uint32_t sh = lo - lo_al;
+#pragma unroll
+  for (int i = 0; i < NCH; i++)
+#pragma unroll
+    for (int j = 0; j < VPL; j++)
+      if (valid(i, j)) {
+        const K key = kv[i * VPL + j];
+        const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
+        const uint32_t sft = (l & 1) * 16;
+        const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sft);
+        staged[sh + ((old >> sft) & 0xFFFFu)] = key;
+      }
+  __syncthreads();
+  // edges: chunk c covers global [lo_al + c*VPL, +VPL) == staged[c*VPL, +VPL)
+  uint4* dst4 = reinterpret_cast<uint4*>(edges + lo_al);
+  const uint4* stg4 = reinterpret_cast<const uint4*>(staged);
+  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
+    const uint32_t g0 = lo_al + c * VPL;
+    if (g0 >= lo && g0 + VPL <= hi) {
+      dst4[c] = stg4[c];
+    } else {
+      for (int j = 0; j < VPL; j++)
+        if (g0 + j >= lo && g0 + j < hi) edges[g0 + j] = staged[c * VPL + j];
+    }
+  }
 }
 
 // Fine bins above the smem capacity: global-memory counters (one 2^s scratch
@@ -750,11 +868,12 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
               unsigned long long* __restrict__ agg) {
   using K = typename H::Key;
   constexpr int QPT = 16;
+  constexpr uint32_t VPL = 16 / sizeof(K);
   constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
-  uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);
-  K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 1) + 15) & ~15u));
+  uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);                        // S + 1 (+ pad to 8)
+  K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 2
   const uint32_t f = blockIdx.x;
   const uint32_t qlo = q_start[f], qhi = q_start[f + 1];
   if (qlo == qhi) return;
@@ -763,35 +882,53 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
   const uint32_t tn = thi - tlo;
   const bool in_smem = tn <= kCap;
+  uint32_t sh = 0;
   if (in_smem) {
-    for (uint32_t i0 = 0; i0 <= nb; i0 += 8 * kT) {
-      uint32_t x[8];
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint32_t i = i0 + k * kT + threadIdx.x;
-        x[k] = i <= nb ? t_off[first + i] : 0u;
+    // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16 relative to tlo
+    const uint4* o4 = reinterpret_cast<const uint4*>(t_off + first);
+    for (uint32_t w = threadIdx.x; 4 * w <= nb; w += blockDim.x) {
+      uint4 x;
+      if (4 * w + 3 <= nb) {
+        x = o4[w];
+      } else {
+        uint32_t t[4] = {0, 0, 0, 0};
+        for (uint32_t e = 0; 4 * w + e <= nb; e++) t[e] = t_off[first + 4 * w + e];
+        x = make_uint4(t[0], t[1], t[2], t[3]);
       }
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint32_t i = i0 + k * kT + threadIdx.x;
-        if (i <= nb) off16[i] = (uint16_t)(x[k] - tlo);
-      }
+      const uint32_t lo2 = ((x.x - tlo) & 0xFFFFu) | ((x.y - tlo) << 16);
+      const uint32_t hi2 = ((x.z - tlo) & 0xFFFFu) | ((x.w - tlo) << 16);
+      reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
     }
-    for (uint32_t j0 = 0; j0 < tn; j0 += 8 * kT) {
-      K x[8];
+    // edges: 16-byte chunks from the boundary below tlo; tedges[sh + j] = edge tlo + j
+    const uint32_t a0 = tlo & ~(VPL - 1);
+    sh = tlo - a0;
+    const uint32_t nch = (thi - a0 + VPL - 1) / VPL;
+    const uint4* e4 = reinterpret_cast<const uint4*>(t_edges + a0);
+    uint4* d4 = reinterpret_cast<uint4*>(tedges);
+    for (uint32_t c0 = 0; c0 < nch; c0 += 4 * kT) {
+      uint4 x[4];
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint32_t j = j0 + k * kT + threadIdx.x;
-        x[k] = j < tn ? t_edges[tlo + j] : K(0);
+      for (int k = 0; k < 4; k++) {
+        const uint32_t c = c0 + k * kT + threadIdx.x;
+        if (c < nch) {
+          if ((c + 1) * VPL + a0 <= thi) {
+            x[k] = e4[c];
+          } else {  // last chunk: do not read past the edge array
+            K t[VPL];
+            for (uint32_t e = 0; e < VPL; e++) t[e] = a0 + c * VPL + e < thi ? t_edges[a0 + c * VPL + e] : K(0);
+            x[k] = *reinterpret_cast<uint4*>(t);
+          }
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint32_t j = j0 + k * kT + threadIdx.x;
-        if (j < tn) tedges[j] = x[k];
+      for (int k = 0; k < 4; k++) {
+        const uint32_t c = c0 + k * kT + threadIdx.x;
+        if (c < nch) d4[c] = x[k];
       }
     }
   }
   __syncthreads();
+  const K* te = tedges + sh;
   uint64_t matched = 0, total = 0, comps = 0;
   for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
     K qv[QPT];
@@ -800,29 +937,38 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
       const uint32_t j = q0 + k * kT + threadIdx.x;
       qv[k] = j < qhi ? qpart[j] : K(0);
     }
+    uint32_t m32 = 0, t32 = 0, c32 = 0;
 #pragma unroll
     for (int k = 0; k < QPT; k++) {
       const uint32_t j = q0 + k * kT + threadIdx.x;
       if (j < qhi) {
         const K q = qv[k];
         const uint32_t h = H::bucket(q, hp);
-        uint32_t a, e, c = 0;
+        uint32_t c;
         if (in_smem) {
           const uint32_t l = h - (uint32_t)first;
-          a = off16[l];
-          e = off16[l + 1];
-          for (uint32_t t = a; t < e; t++) c += (tedges[t] == q);
+          const uint32_t a = off16[l], e = off16[l + 1];
+          const uint32_t d = e - a;
+          // IntersectArray over the bucket: the first two slots without a branch
+          // (buckets hold ~1 key at C = 1), the rest in a loop
+          const K e0 = te[a], e1 = te[a + 1];
+          c = (uint32_t)(d > 0 && e0 == q) + (uint32_t)(d > 1 && e1 == q);
+          for (uint32_t t = a + 2; t < e; t++) c += (te[t] == q);
+          c32 += d;
         } else {
-          a = t_off[h];
-          e = t_off[h + 1];
+          const uint32_t a = t_off[h], e = t_off[h + 1];
+          c = 0;
           for (uint32_t t = a; t < e; t++) c += (t_edges[t] == q);
+          comps += e - a;
         }
         mult_bo[j] = c;
-        matched += (c != 0);
-        total += c;
-        comps += e - a;
+        m32 += (c != 0);
+        t32 += c;
       }
     }
+    matched += m32;
+    total += t32;
+    comps += c32;
   }
   if (agg) flush_agg(matched, total, comps, agg);
 }
@@ -833,11 +979,11 @@ static size_t part_smem(int key_bits) {
   return key_bits == 32 ? sizeof(PartSmem<uint32_t>) : sizeof(PartSmem<uint64_t>);
 }
 static size_t local_smem(int s, int key_bits) {
-  return (size_t)(1u << s) / 2 * 4 + (key_bits == 32 ? LocalShape<uint32_t>::kCap * 4 : LocalShape<uint64_t>::kCap * 8);
+  return (size_t)(1u << s) / 2 * 4 + (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 : (LocalShape<uint64_t>::kCap + 4) * 8);
 }
 static size_t probe_smem(int s, int key_bits) {
-  return (size_t)((2 * ((1u << s) + 1) + 15) & ~15u) +
-         (key_bits == 32 ? LocalShape<uint32_t>::kCap * 4 : LocalShape<uint64_t>::kCap * 8);
+  return (size_t)((2 * ((1u << s) + 8) + 15) & ~15u) +
+         (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 : (LocalShape<uint64_t>::kCap + 4) * 8);
 }
 static size_t unpart_smem() { return (8192 + 3 * kSub + 2) * 4; }
 
@@ -889,7 +1035,7 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   po->tp = ws.take<uint32_t>(L.nb1 + 1);
   po->big_count = ws.take<uint32_t>(64);
   po->M = ws.take<uint32_t>((size_t)L.grid * L.nb1);
-  K* out1 = ws.take<K>(n);
+  K* out1 = ws.take<K>(n + 16 / sizeof(K));  // + tail padding for k_part2's TMA
   K* out2 = nullptr;
   po->out1 = out1;
   po->pmap1 = po->pmap2 = nullptr;
@@ -991,39 +1137,43 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyO
   return HG_OK;
 }
 
+// Host dispatch to the compile-time hasher (reduction mode x hash kind).
+template <typename K, int KIND, typename F>
+static int with_mode(const HashParams& hp, F&& f) {
+  switch (hp.mode) {
+    case kMask:
+      return f(Hasher<K, kMask, KIND>{});
+    case kNone:
+      if constexpr (sizeof(K) == 4) return f(Hasher<K, kNone, KIND>{});
+      [[fallthrough]];
+    case kFastmod:
+      if constexpr (sizeof(K) == 4) return f(Hasher<K, kFastmod, KIND>{});
+      [[fallthrough]];
+    default:
+      return f(Hasher<K, kGeneric64, KIND>{});
+  }
+}
+
+template <typename K, typename F>
+static int with_hasher(const HashParams& hp, F&& f) {
+  if (hp.kind == HG_KIND_IDENTITY) return with_mode<K, HG_KIND_IDENTITY>(hp, f);
+  return with_mode<K, HG_KIND_MURMUR32>(hp, f);
+}
+
 template <typename K>
 int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
                  K* edges, Workspace& ws, cudaStream_t st) {
-  switch (hp.mode) {
-    case kMask:
-      return build_impl<Hasher<K, kMask>>(keys, n, hp, v, L, offsets, edges, ws, st);
-    case kNone:
-      if constexpr (sizeof(K) == 4) return build_impl<Hasher<K, kNone>>(keys, n, hp, v, L, offsets, edges, ws, st);
-      [[fallthrough]];
-    case kFastmod:
-      if constexpr (sizeof(K) == 4) return build_impl<Hasher<K, kFastmod>>(keys, n, hp, v, L, offsets, edges, ws, st);
-      [[fallthrough]];
-    default:
-      return build_impl<Hasher<K, kGeneric64>>(keys, n, hp, v, L, offsets, edges, ws, st);
-  }
+  return with_hasher<K>(hp, [&](auto h) {
+    return build_impl<decltype(h)>(keys, n, hp, v, L, offsets, edges, ws, st);
+  });
 }
 
 template <typename K>
 int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
                  uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
-  switch (hp.mode) {
-    case kMask:
-      return query_impl<Hasher<K, kMask>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
-    case kNone:
-      if constexpr (sizeof(K) == 4) return query_impl<Hasher<K, kNone>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
-      [[fallthrough]];
-    case kFastmod:
-      if constexpr (sizeof(K) == 4)
-        return query_impl<Hasher<K, kFastmod>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
-      [[fallthrough]];
-    default:
-      return query_impl<Hasher<K, kGeneric64>>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
-  }
+  return with_hasher<K>(hp, [&](auto h) {
+    return query_impl<decltype(h)>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+  });
 }
 
 template int binned_build<uint32_t>(const uint32_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,

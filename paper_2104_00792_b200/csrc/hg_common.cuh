@@ -124,11 +124,20 @@ __device__ __forceinline__ uint64_t hash_mod(K key, const HashParams& hp) {
 
 // Compile-time specialised hasher: MODE fixes the reduction (kMask, kFastmod,
 // kNone, kGeneric64) so the hot loops carry no per-key dispatch.
-template <typename K, int MODE>
+template <typename K, int MODE, int KIND = HG_KIND_MURMUR32>
 struct Hasher {
   using Key = K;
+  static __device__ __forceinline__ uint64_t mix(K key, const HashParams& hp) {
+    if constexpr (KIND == HG_KIND_IDENTITY) {
+      return (uint64_t)key;
+    } else if constexpr (sizeof(K) == 4) {
+      return (uint64_t)fmix32((uint32_t)key ^ hp.seed);
+    } else {
+      return fmix64((uint64_t)key ^ (uint64_t)hp.seed);
+    }
+  }
   static __device__ __forceinline__ uint32_t bucket(K key, const HashParams& hp) {
-    const uint64_t x = mix_key(key, hp);
+    const uint64_t x = mix(key, hp);
     if constexpr (MODE == kMask) {
       return (uint32_t)(x & hp.mask);
     } else if constexpr (MODE == kNone) {
@@ -173,6 +182,38 @@ __device__ __forceinline__ uint64_t div_by(uint64_t h, const DivParams& p) {
   if (p.shift >= 0) return h >> p.shift;
   if (h <= 0xFFFFFFFFull && p.d <= 0xFFFFFFFFull) return __umul64hi(p.magic, h);
   return h / p.d;
+}
+
+// --------------------------------------------------------------------------- TMA (1-D bulk copies)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+// Order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses of the same memory.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One thread: expect `bytes` on `bar` and start a global->shared bulk copy
+// (16-byte aligned addresses, size a multiple of 16).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // --------------------------------------------------------------------------- misc

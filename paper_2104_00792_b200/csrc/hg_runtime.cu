@@ -48,6 +48,18 @@ static cudaEvent_t take_event() {
   return e;
 }
 
+// Inside CUDA-graph capture a plain cudaEventRecord would only order work;
+// cudaEventRecordExternal makes it an event-record node that timestamps every
+// replay, so per-kernel timing also works for graph-launched steps.
+static void record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  if (st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 void note_launch_begin(const char* name, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_timing) return;
@@ -55,12 +67,12 @@ void note_launch_begin(const char* name, cudaStream_t s) {
   t_open.name = name;
   t_open.start = take_event();
   t_open.stop = take_event();
-  cudaEventRecord(t_open.start, s);
+  record(t_open.start, s);
 }
 
 void note_launch_end(cudaStream_t s) {
   if (!g_timing || t_open.name == nullptr) return;
-  cudaEventRecord(t_open.stop, s);
+  record(t_open.stop, s);
   std::lock_guard<std::mutex> lk(g_tmu);
   g_records.push_back(t_open);
   t_open = TimingRecord{nullptr, nullptr, nullptr};
