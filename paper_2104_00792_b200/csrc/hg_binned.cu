@@ -351,32 +351,38 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
 
 // --------------------------------------------------------------------------- partition
 
+// Runs are staged in smem at positions congruent (mod 4 elements) to their
+// global destination, so the aligned body of every run leaves with one TMA
+// bulk store: bin b's run starts at pt[b] = toff[b] + 4b + ((dst[b] - toff[b]) & 3).
+constexpr uint32_t kPadMod = 4;
+
 template <typename K>
 struct PartSmem {
-  K raw[TileShape<K>::kTile + 16 / sizeof(K)];  // TMA landing buffer (next tile)
-  K staged[TileShape<K>::kTile];
-  uint8_t bin_at[TileShape<K>::kTile];  // bin of each staged slot
+  K raw[TileShape<K>::kTile + 16 / sizeof(K)];              // TMA landing buffer (next tile)
+  K staged[TileShape<K>::kTile + kPadMod * kSub + 2 * kPadMod];  // runs, padded for alignment
   uint32_t wcnt[kW][kSub];  // per-warp counts -> per-warp slot bases
-  uint32_t toff[kSub + 1];  // tile offsets per bin
+  uint32_t toff[kSub + 1];  // tile offsets per bin (unpadded)
+  uint32_t pt[kSub];        // padded staged start per bin
   uint32_t dst[kSub];       // global write base per bin
-  uint32_t delta[kSub];     // dst - toff: global index of staged slot j is delta[bin] + j
   uint32_t tp[kSub + 1];    // level-2 tile prefix (P2 only)
-  alignas(8) uint64_t bar;  // TMA completion barrier
+  alignas(8) uint64_t bar;  // TMA load barrier
 };
 
-// Rank a register tile by bin and stage it grouped by bin in smem.  Each key
-// takes its rank from one atomic on its warp's private bin counter (the rank
-// stays in registers); a per-bin prefix over warps then gives every key its
-// staged slot.  Afterwards s.toff holds the tile offsets.  pmap (optional)
-// receives each key's staged position, indexed by its tile element.
+__device__ __forceinline__ uint32_t pad_start(uint32_t toff, uint32_t b, uint32_t dst) {
+  return toff + kPadMod * b + ((dst - toff) & (kPadMod - 1));
+}
+
+// Rank a register tile by bin: one atomic on the warp's private bin counter
+// per key (rank kept in registers), then a per-bin prefix over warps.  On
+// return s.wcnt[w][b] is warp w's offset inside bin b's run and s.toff the
+// tile offsets (s.toff[nb] = tile size).
 template <typename K, int KPT, bool kFull>
-__device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT], const uint32_t (&bp)[KPT / 4],
-                                               uint32_t m, uint32_t nb, uint16_t* __restrict__ pmap) {
+__device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[KPT / 4], uint32_t (&rk)[KPT / 2],
+                                          uint32_t m, uint32_t nb) {
   constexpr bool vec = kFull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t b = lane; b < nb; b += 32) s.wcnt[warp][b] = 0;
   __syncwarp();
-  uint32_t rk[KPT / 2];  // 16-bit ranks, two per register
 #pragma unroll
   for (int k = 0; k < KPT; k++) {
     const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
@@ -398,12 +404,29 @@ __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT
   __syncthreads();
   const uint32_t total = block_exscan(s.toff, nb);
   if (threadIdx.x == 0) s.toff[nb] = total;
+  __syncthreads();
+}
+
+// Given s.dst, compute each bin's padded staged start and turn the warp
+// offsets into absolute staged slots.
+__device__ __forceinline__ void pad_bases(uint32_t* pt, uint32_t (*wcnt)[kSub], const uint32_t* toff,
+                                          const uint32_t* dst, uint32_t nb) {
   if (threadIdx.x < nb) {
-    const uint32_t base = s.toff[threadIdx.x];
+    const uint32_t b = threadIdx.x;
+    const uint32_t p = pad_start(toff[b], b, dst[b]);
+    pt[b] = p;
 #pragma unroll
-    for (int w = 0; w < kW; w++) s.wcnt[w][threadIdx.x] += base;
+    for (int w = 0; w < kW; w++) wcnt[w][b] += p;
   }
   __syncthreads();
+}
+
+// Stage every key at its padded slot; pmap (optional) gets the slot.
+template <typename K, int KPT, bool kFull>
+__device__ __forceinline__ void place_tile(PartSmem<K>& s, const K (&kv)[KPT], const uint32_t (&bp)[KPT / 4],
+                                           const uint32_t (&rk)[KPT / 2], uint32_t m, uint16_t* __restrict__ pmap) {
+  constexpr bool vec = kFull;
+  const int warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < KPT; k++) {
     const uint32_t e = tile_elem<K>(k, vec);
@@ -411,27 +434,41 @@ __device__ __forceinline__ void rank_and_stage(PartSmem<K>& s, const K (&kv)[KPT
       const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
       const uint32_t slot = s.wcnt[warp][b] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
       s.staged[slot] = kv[k];
-      s.bin_at[slot] = (uint8_t)b;
       if (pmap) pmap[e] = (uint16_t)slot;
     }
   }
+  fence_proxy_async();  // staged (generic writes) -> TMA bulk-store reads
   __syncthreads();
 }
 
-// Write the staged tile: slot j goes to out[delta[bin_at[j]] + j].  Threads
-// walk consecutive slots, so each warp store covers one or two runs.
-template <typename K, int KPT>
-__device__ __forceinline__ void write_out(const PartSmem<K>& s, uint32_t m, K* __restrict__ out) {
-#pragma unroll
-  for (int k = 0; k < KPT; k++) {
-    const uint32_t j = k * kT + threadIdx.x;
-    if (j < m) out[s.delta[s.bin_at[j]] + j] = s.staged[j];
+// One thread per bin: the unaligned head/tail (< 4 keys each) with plain
+// stores, the aligned body with one TMA bulk store.
+template <typename K>
+__device__ __forceinline__ void store_runs(const PartSmem<K>& s, uint32_t nb, K* __restrict__ out) {
+  if (threadIdx.x < nb) {
+    const uint32_t b = threadIdx.x;
+    const uint32_t cnt = s.toff[b + 1] - s.toff[b];
+    if (cnt) {
+      const uint32_t g = s.dst[b], p = s.pt[b];
+      const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
+      const uint32_t body = (cnt - h) & ~(kPadMod - 1);
+      for (uint32_t i = 0; i < h; i++) out[g + i] = s.staged[p + i];
+#ifdef HG_NO_TMA_STORE
+      for (uint32_t i = h; i < h + body; i++) out[g + i] = s.staged[p + i];
+#else
+      if (body) {
+        tma_store_1d(out + g + h, s.staged + p + h, body * (uint32_t)sizeof(K));
+        tma_store_commit();
+      }
+#endif
+      for (uint32_t i = h + body; i < cnt; i++) out[g + i] = s.staged[p + i];
+    }
   }
 }
 
 // Level 1: CTA chunk tiles, bin = bucket >> shift1, deterministic bases
 // (column-scanned per-CTA counts).  Query mode also records the u16 staged
-// position of every key (pmap) and each tile's offsets (meta, nb+1 words).
+// slot of every key (pmap) and each tile's offsets (meta, nb+1 words).
 template <typename H, bool kQuery>
 __global__ void __launch_bounds__(kT, 2)
 k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1, int bits1, uint32_t nb1, uint64_t chunk,
@@ -482,19 +519,23 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= (b & 0xFFu) << ((k & 3) * 8);
     }
+    if (threadIdx.x < nb1) tma_store_wait_read();  // previous tile's runs have left smem
     fence_proxy_async();
-    __syncthreads();  // raw consumed, previous tile fully written out
+    __syncthreads();  // raw consumed, staged free
     if (threadIdx.x == 0 && tma && t0 + 2 * TS::kTile <= hi)
       tma_load_1d(s.raw, keys + t0 + TS::kTile, TS::kTile * sizeof(K), &s.bar);
-    if (vec) rank_and_stage<K, KPT, true>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
-    else rank_and_stage<K, KPT, false>(s, kv, bp, m, nb1, kQuery ? pmap + t0 : nullptr);
-    if (threadIdx.x < nb1) s.delta[threadIdx.x] = s.dst[threadIdx.x] - s.toff[threadIdx.x];
+    uint32_t rk[KPT / 2];
+    if (vec) rank_tile<K, KPT, true>(s, bp, rk, m, nb1);
+    else rank_tile<K, KPT, false>(s, bp, rk, m, nb1);
+    pad_bases(s.pt, s.wcnt, s.toff, s.dst, nb1);
+    if (vec) place_tile<K, KPT, true>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
+    else place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     if (kQuery)
       for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) meta[(t0 / TS::kTile) * (nb1 + 1) + i] = s.toff[i];
-    __syncthreads();
-    write_out<K, KPT>(s, m, out);
+    store_runs<K>(s, nb1, out);
     if (threadIdx.x < nb1) s.dst[threadIdx.x] += s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
   }
+  if (threadIdx.x < nb1) tma_store_wait_all();
 }
 
 // Level 2: tiles of each level-1 bin, sub-bin = fine & 127, space claimed per
@@ -560,6 +601,7 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= b << ((k & 3) * 8);
     }
+    if (threadIdx.x < kSub) tma_store_wait_read();
     fence_proxy_async();
     __syncthreads();
     if (threadIdx.x == 0 && t + gridDim.x < ntiles) {
@@ -567,47 +609,58 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
       locate(t + gridDim.x, c2, t02, m2);
       issue(t02, m2);
     }
-    rank_and_stage<K, KPT, false>(s, kv, bp, m, kSub, kQuery ? pmap + t0 : nullptr);
+    uint32_t rk[KPT / 2];
+    rank_tile<K, KPT, false>(s, bp, rk, m, kSub);
     if (threadIdx.x < kSub) {
       const uint32_t cnt = s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
       const uint32_t d = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
-      s.delta[threadIdx.x] = d - s.toff[threadIdx.x];
+      s.dst[threadIdx.x] = d;
       if (kQuery) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = d;
     }
     if (kQuery)
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
     __syncthreads();
-    write_out<K, KPT>(s, m, out);
+    pad_bases(s.pt, s.wcnt, s.toff, s.dst, kSub);
+    place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
+    store_runs<K>(s, kSub, out);
   }
+  if (threadIdx.x < kSub) tma_store_wait_all();
 }
 
 // Reverse of a partition level for per-query uint32 values.  Level 2: tiles
 // from the level-2 tile table, run bases from meta; level 1: each CTA replays
-// its chunk's tiles with cursors from the column-scanned counts.  Runs are
-// pulled into smem in staged order, then out[i] = staged[pmap[i]].
+// its chunk's tiles with cursors from the column-scanned counts.  Each run is
+// pulled back into its padded staged slot range (TMA for the aligned body),
+// then out[i] = staged[pmap[i]].
 template <int kLevel>
 __global__ void __launch_bounds__(kT, 2)
 k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
          const uint32_t* __restrict__ meta, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
          const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
-  constexpr int VPT = 8192 / kT;  // staged values per thread
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw);  // tile <= 8192
-  uint32_t* toff = staged + 8192;                         // kSub + 1
-  uint32_t* base = toff + kSub + 1;                       // kSub
-  uint32_t* tps = base + kSub;                            // kSub + 1
+  constexpr int VPT = 8192 / kT;  // gathered values per thread (tile <= 8192)
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);
+  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + 16);  // 8192 + 4*kSub + 8
+  uint32_t* toff = staged + 8192 + kPadMod * kSub + 2 * kPadMod;  // kSub + 1
+  uint32_t* base = toff + kSub + 1;                              // kSub
+  uint32_t* tps = base + kSub;                                   // kSub + 1
   uint64_t lo = 0, hi = 0;
   uint32_t ntiles = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_proxy_async();
+  }
   if (kLevel == 1) {
     lo = (uint64_t)blockIdx.x * chunk;
     hi = min(n, lo + chunk);
     if (threadIdx.x < nb) base[threadIdx.x] = c_start[threadIdx.x] + M[(uint64_t)blockIdx.x * nb + threadIdx.x];
   } else {
     for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) tps[i] = tp_g[i];
-    __syncthreads();
-    ntiles = tps[nb];
   }
+  __syncthreads();
+  if (kLevel == 2) ntiles = tps[nb];
   const uint32_t nbb = kLevel == 1 ? nb : kSub;
+  uint32_t parity = 0;
   for (uint64_t it = (kLevel == 1 ? lo : blockIdx.x);; it += (kLevel == 1 ? tile : gridDim.x)) {
     uint32_t m;
     uint64_t t0, tix;
@@ -628,7 +681,8 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       m = min(tile, c_start[a + 1] - (uint32_t)t0);
       tix = t;
     }
-    __syncthreads();
+    fence_proxy_async();
+    __syncthreads();  // previous gather done: staged is free
     if (kLevel == 1) {
       for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) toff[i] = meta[tix * (nb + 1) + i];
     } else {
@@ -636,53 +690,38 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) toff[i] = meta[tix * (2 * kSub + 1) + kSub + i];
     }
     __syncthreads();
-    {
-      // warp w gathers staged positions [w*VPT*32, (w+1)*VPT*32): find the bin
-      // of its first position once, then each lane walks forward (runs are
-      // ~tile/nb long, so a lane crosses at most a few run starts)
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      const uint32_t j0 = (uint32_t)warp * VPT * 32;
-      uint32_t lo_b = 0, hi_b = nbb;  // last b with toff[b] <= j0
-      while (hi_b - lo_b > 1) {
-        const uint32_t mid = (lo_b + hi_b) >> 1;
-        if (toff[mid] <= j0) lo_b = mid; else hi_b = mid;
-      }
-      uint32_t b = lo_b;
-      uint32_t v[VPT];
-#pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        const uint32_t j = j0 + k * 32 + lane;
-        uint32_t x = 0;
-        if (j < m) {
-          while (toff[b + 1] <= j) b++;
-          x = vals[(int64_t)base[b] - (int64_t)toff[b] + j];
+    if (threadIdx.x < nbb) {
+      const uint32_t b = threadIdx.x;
+      const uint32_t cnt = toff[b + 1] - toff[b];
+      if (cnt) {
+        const uint32_t g = base[b];
+        const uint32_t p = pad_start(toff[b], b, g);
+        const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
+        const uint32_t body = (cnt - h) & ~(kPadMod - 1);
+        if (body) {
+          mbar_expect_tx(bar, body * 4);
+          tma_load_1d_tx(staged + p + h, vals + g + h, body * 4, bar);
         }
-        v[k] = x;
-      }
-#pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        const uint32_t j = j0 + k * 32 + lane;
-        if (j < m) staged[j] = v[k];
+        for (uint32_t i = 0; i < h; i++) staged[p + i] = vals[g + i];
+        for (uint32_t i = h + body; i < cnt; i++) staged[p + i] = vals[g + i];
       }
     }
     __syncthreads();
-    {
-      uint32_t pm[VPT];  // position maps first (all loads in flight), then the smem gathers
+    if (threadIdx.x == 0) mbar_arrive(bar);
+    uint32_t pm[VPT];  // position maps load while the runs land
 #pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        const uint32_t i = k * kT + threadIdx.x;
-        pm[k] = i < m ? pmap[t0 + i] : 0u;
-      }
+    for (int k = 0; k < VPT; k++) {
+      const uint32_t i = k * kT + threadIdx.x;
+      pm[k] = i < m ? pmap[t0 + i] : 0u;
+    }
+    mbar_wait(bar, parity);
+    parity ^= 1;
 #pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        const uint32_t i = k * kT + threadIdx.x;
-        if (i < m) out[t0 + i] = staged[pm[k]];
-      }
+    for (int k = 0; k < VPT; k++) {
+      const uint32_t i = k * kT + threadIdx.x;
+      if (i < m) out[t0 + i] = staged[pm[k]];
     }
-    if (kLevel == 1) {
-      __syncthreads();
-      if (threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
-    }
+    if (kLevel == 1 && threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
   }
 }
 
@@ -985,7 +1024,7 @@ static size_t probe_smem(int s, int key_bits) {
   return (size_t)((2 * ((1u << s) + 8) + 15) & ~15u) +
          (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 : (LocalShape<uint64_t>::kCap + 4) * 8);
 }
-static size_t unpart_smem() { return (8192 + 3 * kSub + 2) * 4; }
+static size_t unpart_smem() { return (8192 + kPadMod * kSub + 2 * kPadMod + 3 * kSub + 4) * 4 + 16; }
 
 size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query) {
   const size_t kb = key_bits / 8;
