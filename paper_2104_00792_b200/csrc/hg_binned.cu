@@ -177,6 +177,50 @@ __device__ void block_exscan_u16(uint32_t* w16, uint32_t nvals) {
   __syncthreads();
 }
 
+// Exclusive scan of n uint32 in smem (in place), warp-row layout (no bank
+// conflicts); `base` is added to every output.  Returns the total.
+__device__ uint32_t block_exscan_rows(uint32_t* a, uint32_t n, uint32_t base) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t seg = ((n + nw - 1) / nw + 31) & ~31u;
+  const uint32_t w0 = warp * seg, w1 = min(w0 + seg, n);
+  uint32_t part = 0;
+  for (uint32_t i = w0 + lane; i < w1; i += 32) part += a[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) s_w[warp] = part;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < nw ? s_w[lane] : 0u;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane < nw) s_w[lane] = inc - x;
+    if (lane == 31) s_total = inc;
+  }
+  __syncthreads();
+  const uint32_t total = s_total;
+  uint32_t carry = base + s_w[warp];
+  for (uint32_t r = w0; r < w1; r += 32) {
+    const uint32_t i = r + lane;
+    const uint32_t x = i < w1 ? a[i] : 0u;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (i < w1) a[i] = carry + inc - x;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __syncthreads();
+  return total;
+}
+
 // Inclusive max-scan of n (<= 32 * blockDim) uint32 in smem, in place.
 __device__ void block_maxscan(uint32_t* a, uint32_t n) {
   __shared__ uint32_t s_w[32];
@@ -819,18 +863,21 @@ k_local_build(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint
   }
 }
 
-// Fine bins above the smem capacity: global-memory counters (one 2^s scratch
-// per CTA).  When `copy` is set the bin is first copied from `edges` into
-// `src` (same offsets) so placement can overwrite edges.
+// Fine bins above the smem capacity (high-duplicate inputs): the bin's keys
+// stream from global memory twice while the 2^s counters stay in smem; lanes
+// of a warp that hit the same bucket (the common case here) share one atomic.
+// When `copy` is set the bin is first copied from `edges` into `src` (same
+// offsets) so placement can overwrite edges.
 template <typename H>
 __global__ void __launch_bounds__(1024)
 k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
                   const uint32_t* __restrict__ big_count, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ scratch,
                   uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
   using K = typename H::Key;
+  (void)scratch;
+  extern __shared__ uint32_t cnt[];  // 2^s counters
   const uint32_t S = 1u << s;
-  uint32_t* cnt = scratch + (uint64_t)blockIdx.x * S;
-  __shared__ uint32_t s_w[32];
+  const int lane = threadIdx.x & 31;
   for (uint32_t k = blockIdx.x; k < *big_count; k += gridDim.x) {
     const uint32_t f = big_list[k];
     const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
@@ -840,40 +887,38 @@ k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_sta
       for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) src[j] = edges[j];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(cnt + (H::bucket(src[j], hp) - (uint32_t)first), 1u);
-    __syncthreads();
-    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
-    const uint32_t a0 = threadIdx.x * per, a1 = min(a0 + per, nb);
-    uint32_t sum = 0;
-    for (uint32_t i = a0; i < a1; i++) sum += cnt[i];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t inc = sum;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_w[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = lane < nw ? s_w[lane] : 0u;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
+    const uint32_t rounds = (hi - lo + blockDim.x - 1) / blockDim.x;
+    for (uint32_t r = 0; r < rounds; r++) {
+      const uint32_t j = lo + r * blockDim.x + threadIdx.x;
+      const bool ok = j < hi;
+      const uint32_t l = ok ? H::bucket(src[j], hp) - (uint32_t)first : 0u;
+      const uint32_t act = __ballot_sync(0xffffffffu, ok);
+      const uint32_t l0 = __shfl_sync(0xffffffffu, l, act ? __ffs(act) - 1 : 0);
+      if (__all_sync(0xffffffffu, !ok || l == l0)) {
+        if (act && lane == __ffs(act) - 1) atomicAdd(cnt + l0, (uint32_t)__popc(act));
+      } else if (ok) {
+        atomicAdd(cnt + l, 1u);
       }
-      if (lane < nw) s_w[lane] = w;
     }
     __syncthreads();
-    uint32_t run = lo + (warp ? s_w[warp - 1] : 0u) + inc - sum;
-    for (uint32_t i = a0; i < a1; i++) {
-      const uint32_t x = cnt[i];
-      cnt[i] = run;
-      offsets[first + i] = run;
-      run += x;
-    }
+    block_exscan_rows(cnt, nb, lo);
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = cnt[i];
     __syncthreads();
-    for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-      const K key = src[j];
-      edges[atomicAdd(cnt + (H::bucket(key, hp) - (uint32_t)first), 1u)] = key;
+    for (uint32_t r = 0; r < rounds; r++) {
+      const uint32_t j = lo + r * blockDim.x + threadIdx.x;
+      const bool ok = j < hi;
+      const K key = ok ? src[j] : K(0);
+      const uint32_t l = ok ? H::bucket(key, hp) - (uint32_t)first : 0u;
+      const uint32_t act = __ballot_sync(0xffffffffu, ok);
+      const uint32_t l0 = __shfl_sync(0xffffffffu, l, act ? __ffs(act) - 1 : 0);
+      if (__all_sync(0xffffffffu, !ok || l == l0)) {
+        uint32_t b0 = 0;
+        if (act && lane == __ffs(act) - 1) b0 = atomicAdd(cnt + l0, (uint32_t)__popc(act));
+        b0 = __shfl_sync(0xffffffffu, b0, act ? __ffs(act) - 1 : 0);
+        if (ok) edges[b0 + __popc(act & lanemask_lt())] = key;
+      } else if (ok) {
+        edges[atomicAdd(cnt + l, 1u)] = key;
+      }
     }
     __syncthreads();
   }
@@ -895,6 +940,141 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
   }
 }
 
+// ---- small per-CTA map for deep buckets (high-duplicate inputs)
+constexpr uint32_t kBigDeg = 16;     // buckets deeper than this use the map
+constexpr uint32_t kMapSlots = 256;  // open addressing, power of two
+
+template <typename K>
+struct BigMap {
+  K key[kMapSlots];
+  uint32_t cnt[kMapSlots];
+  uint32_t state[kMapSlots];  // 0 empty, 1 claiming, 2 ready
+  uint32_t full;
+};
+
+template <typename K>
+__device__ __forceinline__ void map_clear(BigMap<K>& m) {
+  for (uint32_t i = threadIdx.x; i < kMapSlots; i += blockDim.x) {
+    m.state[i] = 0;
+    m.cnt[i] = 0;
+  }
+  if (threadIdx.x == 0) m.full = 0;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t map_slot(K key) {
+  return (uint32_t)(fmix64((uint64_t)key) & (kMapSlots - 1));
+}
+
+// Add one occurrence of `key` (lanes with ok == false only join the warp
+// aggregation); equal keys inside a warp are merged with one atomic.
+template <typename K>
+__device__ __forceinline__ void map_add(BigMap<K>& m, K key, bool ok) {
+  const uint32_t act = __ballot_sync(0xffffffffu, ok);
+  if (!act) return;
+  const int first_lane = __ffs(act) - 1;
+  const K k0 = __shfl_sync(0xffffffffu, key, first_lane);
+  const bool same = __all_sync(0xffffffffu, !ok || key == k0);  // deep buckets: usually one key
+  if (!ok) return;
+  uint32_t peers;
+  if (same) {
+    peers = act;
+  } else {
+    peers = __match_any_sync(act, key);
+  }
+  if ((threadIdx.x & 31) != __ffs(peers) - 1) return;
+  const uint32_t add = __popc(peers);
+  uint32_t i = map_slot(key);
+  for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
+    uint32_t st = atomicCAS(&m.state[i], 0u, 1u);
+    if (st == 0) {  // claimed an empty slot
+      m.key[i] = key;
+      __threadfence_block();
+      atomicExch(&m.state[i], 2u);
+      atomicAdd(&m.cnt[i], add);
+      return;
+    }
+    while (st == 1) st = atomicAdd(&m.state[i], 0u);  // another lane is publishing this slot
+    if (*reinterpret_cast<volatile const K*>(&m.key[i]) == key) {
+      atomicAdd(&m.cnt[i], add);
+      return;
+    }
+  }
+  m.full = 1;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t map_count(const BigMap<K>& m, K key) {
+  uint32_t i = map_slot(key);
+  for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
+    if (m.state[i] == 0) return 0;
+    if (m.key[i] == key) return m.cnt[i];
+  }
+  return 0;
+}
+
+// The bin's queries, 16 per thread per batch (loads first), each answered by
+// IntersectArray over its bucket (kSmem: the staged slice; else global
+// memory) or by the deep-bucket map.
+template <typename H, bool kSmem>
+__device__ __forceinline__ void probe_queries(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
+                                              const HashParams& hp, uint32_t first, const uint16_t* off16,
+                                              const KeyOf<H>* te, const uint32_t* __restrict__ t_off,
+                                              const KeyOf<H>* __restrict__ t_edges, uint32_t tlo,
+                                              const BigMap<KeyOf<H>>& map, bool overflow, uint32_t* __restrict__ mult_bo,
+                                              uint64_t& matched, uint64_t& total, uint64_t& comps) {
+  using K = typename H::Key;
+  constexpr int QPT = 16;
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
+    K qv[QPT];
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      const uint32_t j = q0 + k * kT + threadIdx.x;
+      qv[k] = j < qhi ? qpart[j] : K(0);
+    }
+    uint32_t m32 = 0, t32 = 0;
+    uint64_t c64 = 0;
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      const uint32_t j = q0 + k * kT + threadIdx.x;
+      if (j < qhi) {
+        const K q = qv[k];
+        const uint32_t h = H::bucket(q, hp);
+        uint32_t a, e, c;
+        if (kSmem) {
+          a = off16[h - first];
+          e = off16[h - first + 1];
+        } else {
+          a = t_off[h] - tlo;
+          e = t_off[h + 1] - tlo;
+        }
+        const uint32_t d = e - a;
+        if (d > kBigDeg && !overflow) {
+          c = map_count(map, q);
+        } else if (kSmem) {
+          // the first two slots without a branch (buckets hold ~1 key at C = 1)
+          const K e0 = te[a], e1 = te[a + 1];
+          c = (uint32_t)(d > 0 && e0 == q) + (uint32_t)(d > 1 && e1 == q);
+          for (uint32_t t = a + 2; t < e; t += 2) {  // two slots per trip (one may be past e)
+            const K x0 = te[t], x1 = te[t + 1];
+            c += (uint32_t)(x0 == q) + (uint32_t)(t + 1 < e && x1 == q);
+          }
+        } else {
+          c = 0;
+          for (uint32_t t = a; t < e; t++) c += (t_edges[tlo + t] == q);
+        }
+        mult_bo[j] = c;
+        m32 += (c != 0);
+        t32 += c;
+        c64 += d;
+      }
+    }
+    matched += m32;
+    total += t32;
+    comps += c64;
+  }
+}
+
 // One CTA per fine bin: the table's CSR slice (uint16 local offsets + edges)
 // staged in smem; the bin's queries probe it with IntersectArray semantics
 // (count of equal keys in the bucket; comparisons += bucket
@@ -912,7 +1092,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   extern __shared__ __align__(16) unsigned char s_raw[];
   const uint32_t S = 1u << s;
   uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);                        // S + 1 (+ pad to 8)
-  K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 2
+  K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 8
+  BigMap<K>& map = *reinterpret_cast<BigMap<K>*>(reinterpret_cast<unsigned char*>(tedges) + (kCap + 8) * sizeof(K));
   const uint32_t f = blockIdx.x;
   const uint32_t qlo = q_start[f], qhi = q_start[f + 1];
   if (qlo == qhi) return;
@@ -922,9 +1103,14 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const uint32_t tn = thi - tlo;
   const bool in_smem = tn <= kCap;
   uint32_t sh = 0;
+  __shared__ uint32_t s_deep;
+  if (threadIdx.x == 0) s_deep = in_smem ? 0u : 1u;
+  __syncthreads();
   if (in_smem) {
-    // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16 relative to tlo
+    // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16 relative to tlo;
+    // also flag the bin if any bucket is deeper than kBigDeg
     const uint4* o4 = reinterpret_cast<const uint4*>(t_off + first);
+    bool deep = false;
     for (uint32_t w = threadIdx.x; 4 * w <= nb; w += blockDim.x) {
       uint4 x;
       if (4 * w + 3 <= nb) {
@@ -934,10 +1120,16 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
         for (uint32_t e = 0; 4 * w + e <= nb; e++) t[e] = t_off[first + 4 * w + e];
         x = make_uint4(t[0], t[1], t[2], t[3]);
       }
+      // degrees of buckets 4w..4w+3 (only those below nb exist)
+      const uint32_t i0 = 4 * w;
+      const uint32_t nx = i0 + 4 <= nb ? t_off[first + i0 + 4] : 0u;
+      deep |= (i0 + 1 <= nb && x.y - x.x > kBigDeg) | (i0 + 2 <= nb && x.z - x.y > kBigDeg) |
+              (i0 + 3 <= nb && x.w - x.z > kBigDeg) | (i0 + 4 <= nb && nx - x.w > kBigDeg);
       const uint32_t lo2 = ((x.x - tlo) & 0xFFFFu) | ((x.y - tlo) << 16);
       const uint32_t hi2 = ((x.z - tlo) & 0xFFFFu) | ((x.w - tlo) << 16);
       reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
     }
+    if (__any_sync(0xffffffffu, deep) && (threadIdx.x & 31) == 0) s_deep = 1u;
     // edges: 16-byte chunks from the boundary below tlo; tedges[sh + j] = edge tlo + j
     const uint32_t a0 = tlo & ~(VPL - 1);
     sh = tlo - a0;
@@ -968,47 +1160,50 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   }
   __syncthreads();
   const K* te = tedges + sh;
-  uint64_t matched = 0, total = 0, comps = 0;
-  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
-    K qv[QPT];
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t j = q0 + k * kT + threadIdx.x;
-      qv[k] = j < qhi ? qpart[j] : K(0);
-    }
-    uint32_t m32 = 0, t32 = 0, c32 = 0;
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t j = q0 + k * kT + threadIdx.x;
-      if (j < qhi) {
-        const K q = qv[k];
-        const uint32_t h = H::bucket(q, hp);
-        uint32_t c;
+  // Buckets deeper than kBigDeg (high-duplicate inputs) are answered from a
+  // small smem map key -> occurrences, built once per bin, instead of an
+  // O(degree) scan per query.
+  map_clear(map);
+  __syncthreads();
+  if (s_deep) {
+    // each warp scans 32 consecutive buckets per round and feeds the deep
+    // ones (ballot) to the map cooperatively
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t l0 = (uint32_t)warp * 32; l0 < nb; l0 += blockDim.x) {
+      const uint32_t l = l0 + lane;
+      uint32_t a = 0, e = 0;
+      if (l < nb) {
         if (in_smem) {
-          const uint32_t l = h - (uint32_t)first;
-          const uint32_t a = off16[l], e = off16[l + 1];
-          const uint32_t d = e - a;
-          // IntersectArray over the bucket: the first two slots without a branch
-          // (buckets hold ~1 key at C = 1), the rest in a loop
-          const K e0 = te[a], e1 = te[a + 1];
-          c = (uint32_t)(d > 0 && e0 == q) + (uint32_t)(d > 1 && e1 == q);
-          for (uint32_t t = a + 2; t < e; t++) c += (te[t] == q);
-          c32 += d;
+          a = off16[l];
+          e = off16[l + 1];
         } else {
-          const uint32_t a = t_off[h], e = t_off[h + 1];
-          c = 0;
-          for (uint32_t t = a; t < e; t++) c += (t_edges[t] == q);
-          comps += e - a;
+          a = t_off[first + l] - tlo;
+          e = t_off[first + l + 1] - tlo;
         }
-        mult_bo[j] = c;
-        m32 += (c != 0);
-        t32 += c;
+      }
+      uint32_t deep = __ballot_sync(0xffffffffu, e - a > kBigDeg);
+      while (deep) {
+        const int src = __ffs(deep) - 1;
+        deep &= deep - 1;
+        const uint32_t ba = __shfl_sync(0xffffffffu, a, src), be = __shfl_sync(0xffffffffu, e, src);
+        for (uint32_t t0 = ba; t0 < be; t0 += 32) {
+          const uint32_t t = t0 + lane;
+          const bool ok = t < be;
+          const K key = ok ? (in_smem ? te[t] : t_edges[tlo + t]) : K(0);
+          map_add(map, key, ok);
+        }
       }
     }
-    matched += m32;
-    total += t32;
-    comps += c32;
   }
+  __syncthreads();
+  const bool overflow = map.full != 0;
+  uint64_t matched = 0, total = 0, comps = 0;
+  if (in_smem)
+    probe_queries<H, true>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow, mult_bo,
+                           matched, total, comps);
+  else
+    probe_queries<H, false>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow,
+                            mult_bo, matched, total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
 }
 
@@ -1022,7 +1217,8 @@ static size_t local_smem(int s, int key_bits) {
 }
 static size_t probe_smem(int s, int key_bits) {
   return (size_t)((2 * ((1u << s) + 8) + 15) & ~15u) +
-         (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 : (LocalShape<uint64_t>::kCap + 4) * 8);
+         (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 + sizeof(BigMap<uint32_t>)
+                         : (LocalShape<uint64_t>::kCap + 8) * 8 + sizeof(BigMap<uint64_t>));
 }
 static size_t unpart_smem() { return (8192 + kPadMod * kSub + 2 * kPadMod + 3 * kSub + 4) * 4 + 16; }
 
@@ -1143,7 +1339,9 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   // oversized fine bins: with two levels their keys sit in edges (in place), so
   // they are copied to the free level-1 buffer first
   const int copy = L.two_level ? 1 : 0;
-  HG_LAUNCH("hg_local_build_big", k_local_build_big<H>, num_sms(), 1024, 0, st, (K*)po.out1, copy, po.fine_start,
+  const size_t smBig = (size_t)(1u << L.s) * 4;
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_big<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_LAUNCH("hg_local_build_big", k_local_build_big<H>, num_sms(), 1024, smBig, st, (K*)po.out1, copy, po.fine_start,
             po.big_list, po.big_count, hp, L.s, v, scratch, offsets, edges);
   return HG_OK;
 }

@@ -218,3 +218,21 @@ def test_all_identical_keys_large():
     assert table.contains(123456) == n
     res = hg.intersect(table, np.array([123456, 5, 123456], dtype=np.uint32))
     assert res.multiplicities.tolist() == [n, 0, n]
+
+
+@pytest.mark.parametrize("n,values,lf", [(1 << 20, 1 << 8, 1.0), (1 << 22, 1 << 12, 1.0), ((1 << 20) + 5, 3, 2.0)])
+def test_high_duplicate_build_and_query(n, values, lf):
+    """C3-shaped inputs (many copies of few values): deep buckets go through the
+    probe's per-bin map and oversized fine bins through the global build."""
+    rng = np.random.default_rng(values)
+    domain = rng.integers(0, 1 << 32, size=values, dtype=np.uint64).astype(np.uint32)
+    keys = domain[rng.integers(0, values, size=n)]
+    queries = np.concatenate([domain[rng.integers(0, values, size=n // 2)],
+                              rng.integers(0, 1 << 32, size=n // 8, dtype=np.uint64).astype(np.uint32)])
+    table = hg.build(keys, lf)
+    off, placed, _ = O.build_csr(keys, table.hash_range)
+    assert_table_equal(table, off, placed)
+    res = hg.intersect(table, queries)
+    assert np.array_equal(res.multiplicities, O.count_occurrences(keys, queries))
+    _, matched, total, comp, _ = O.query(off, placed, queries)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
