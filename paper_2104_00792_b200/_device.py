@@ -3,6 +3,8 @@ computation is a libhashgraph_b200 kernel launched through _lib."""
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from . import _lib
@@ -108,7 +110,9 @@ def to_device_keys(keys, key_bits: int = 32):
             keys = keys.to(want)
         return keys.to(device(), non_blocking=keys.is_pinned())
     arr = coerce_host_keys(keys, key_bits)
-    host = t.from_numpy(arr.view(np.int32 if key_bits == 32 else np.int64))
+    with warnings.catch_warnings():  # read-only arrays (e.g. a table's keys) are only read here
+        warnings.simplefilter("ignore", UserWarning)
+        host = t.from_numpy(arr.view(np.int32 if key_bits == 32 else np.int64))
     return host.to(device(), non_blocking=False)
 
 
