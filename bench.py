@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--log2-keys", type=int, default=28, help="keys (and queries) per GPU = 2^x")
     ap.add_argument("--k", type=int, default=28, help="keys drawn from {1..2^k}")
     ap.add_argument("--load-factor", type=float, default=1.0)
+    ap.add_argument("--key-bits", type=int, default=32, choices=[32, 64],
+                    help="64: full SplitMix64 words as keys (BASELINE configs[3])")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-log2", type=int, default=24, help="CPU baseline sample size 2^x")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -143,7 +145,7 @@ def algorithmic_bytes(name: str, n: int, q: int, v: int, w: int = 4) -> float:
     return float(table.get(name, 0))
 
 
-def summarize_kernels(records, steps, n, q, v, peak):
+def summarize_kernels(records, steps, n, q, v, peak, w=4):
     agg = {}
     for name, ms in records:
         a = agg.setdefault(name, [0, 0.0])
@@ -153,13 +155,13 @@ def summarize_kernels(records, steps, n, q, v, peak):
     rows = []
     for name, (cnt, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         avg = ms / cnt
-        ab = algorithmic_bytes(name, n, q, v)
+        ab = algorithmic_bytes(name, n, q, v, w)
         rows.append({"kernel": name, "launches": cnt, "avg_ms": avg, "share": ms / total,
                      "achieved_gbs": (ab / (avg / 1e3) / 1e9) if ab else None})
     top = rows[0] if rows else None
     roof = None
     if top:
-        ab = algorithmic_bytes(top["kernel"], n, q, v)
+        ab = algorithmic_bytes(top["kernel"], n, q, v, w)
         ach = ab / (top["avg_ms"] / 1e3) / 1e9 if ab else None
         roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": None, "share_of_step": top["share"],
@@ -252,14 +254,15 @@ def main():
     q = n
     spec = hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, args.k, n, rank)
     qspec = hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, args.k, q * world, QUERY_SEED)
-    keys = hg.generate_device(spec, 0, n)
-    queries = hg.generate_device(qspec, rank * q, q)
+    kb = args.key_bits
+    keys = hg.generate_device(spec, 0, n, key_bits=kb)
+    queries = hg.generate_device(qspec, rank * q, q, key_bits=kb)
     torch.cuda.synchronize()
 
     if world > 1:
         from paper_2104_00792_b200 import distributed as hd
 
-        cfg = hd.DistConfig(load_factor=args.load_factor)
+        cfg = hd.DistConfig(load_factor=args.load_factor, key_bits=kb)
 
         def step():
             table = hd.build_distributed(keys, cfg)
@@ -267,7 +270,7 @@ def main():
             return table, res
     else:
         def step():
-            table = hg.build(keys, args.load_factor)
+            table = hg.build(keys, args.load_factor, key_bits=kb)
             res = hg.intersect(table, queries)
             return table, res
 
@@ -333,7 +336,7 @@ def main():
     value = total_units / (elapsed_ms / 1e3)
 
     peak, peak_kind = measured_peak()
-    kernels, roof = summarize_kernels(records, args.steps, n, q, v, peak)
+    kernels, roof = summarize_kernels(records, args.steps, n, q, v, peak, kb // 8)
     if roof:
         roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback"
         roof["traffic"] = load_traffic(roof["kernel"])
@@ -341,8 +344,9 @@ def main():
     # end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        hk = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        hq = torch.empty(q, dtype=torch.int32, pin_memory=True)
+        sdt = torch.int32 if kb == 32 else torch.int64
+        hk = torch.empty(n, dtype=sdt, pin_memory=True)
+        hq = torch.empty(q, dtype=sdt, pin_memory=True)
         hk.copy_(keys.cpu())
         hq.copy_(queries.cpu())
         out = torch.empty(q, dtype=torch.int32, pin_memory=True)
@@ -352,7 +356,7 @@ def main():
                 table = hd.build_distributed(hk, cfg)
                 res = hd.query_distributed(table, hq)
             else:
-                table = hg.build(hk, args.load_factor)
+                table = hg.build(hk, args.load_factor, key_bits=kb)
                 res = hg.intersect(table, hq)
             out.copy_(res.multiplicities_device, non_blocking=True)
             return res
@@ -371,7 +375,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": (n + q) * world * args.e2e_steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": 4 * (n + q), "d2h_bytes_per_step": 4 * q,
+               "h2d_bytes_per_step": (kb // 8) * (n + q), "d2h_bytes_per_step": 4 * q,
                "ms_per_step": e2e_s / args.e2e_steps * 1e3}
 
     if rank != 0:
@@ -391,9 +395,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": (f"C5 weak scaling: 2^{args.log2_keys} uint32 keys + 2^{args.log2_keys} queries per "
-                                f"GPU, keys from {{1..2^{args.k}}}, C={args.load_factor}"),
+        "scaling": "weak", "vs_baseline": None, "dtype": f"u{kb}", "data": "synthetic",
+        "config": {"workload": (f"C5 weak scaling: 2^{args.log2_keys} uint{kb} keys + 2^{args.log2_keys} queries per "
+                                f"GPU, " + (f"keys from {{1..2^{args.k}}}" if kb == 32 else "full 64-bit SplitMix64 words")
+                                + f", C={args.load_factor}"),
                    "keys_per_gpu": n, "queries_per_gpu": q, "hash_range_per_gpu": v,
                    "l2": "inputs (1 GiB per array) larger than the 126 MB L2",
                    "parallelism": "single-shard" if world == 1 else f"partitioned over {world} GPUs (NCCL)",

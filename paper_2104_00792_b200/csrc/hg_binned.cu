@@ -30,9 +30,10 @@ namespace hg {
 
 constexpr int kT = 512;          // threads per CTA; two CTAs per SM
 constexpr int kW = kT / 32;      // warps per CTA
-constexpr int kSub = 128;        // max bins per partition level (7-bit ballots)
+constexpr int kSub = 128;        // level-2 fan-out (fine bins per level-1 bin)
 constexpr int kSubBits = 7;
-constexpr uint32_t kMaxFine = 16384;
+constexpr int kMaxBins = 256;    // bins one partition tile can split into (8-bit bin ids)
+constexpr uint32_t kMaxFine = kSub * kMaxBins;  // 32768
 
 template <typename K>
 struct TileShape {
@@ -53,17 +54,19 @@ static int ceil_log2(uint32_t x) {
   return b;
 }
 
-static int pick_s(uint64_t n, uint64_t v) {
-  double per_bucket = v ? (double)n / (double)v : 1.0;
+// ~0.85 of the local stages' capacity per fine bin on average
+static int pick_s(uint64_t n, uint64_t v, int key_bits) {
+  const double per_bucket = v ? (double)n / (double)v : 1.0;
+  const double target = key_bits == 32 ? 17000.0 : 8500.0;
   int s = 14;
-  while (s > 6 && per_bucket * (double)(1ull << s) > 17000.0) s--;
+  while (s > 6 && per_bucket * (double)(1ull << s) > target) s--;
   return s;
 }
 
 // n_table sizes the fine bins (a bin's table keys must fit smem); n sizes the chunks.
 bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L) {
   if (v > (1ull << 32)) return false;
-  const int s = pick_s(n_table, v);
+  const int s = pick_s(n_table, v, key_bits);
   const uint64_t F = (v + (1ull << s) - 1) >> s;
   if (F > kMaxFine) return false;
   L->s = s;
@@ -302,7 +305,29 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;
   const uint64_t hi = min(n, lo + chunk);
-  if (sizeof(K) == 4 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
+  if (sizeof(K) == 8 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
+    const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
+    const uint64_t nv = (hi - lo) / 2;
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) q[u] = __ldcs(p + i + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const K* qk = reinterpret_cast<const K*>(&q[u]);
+        atomicAdd(s_h + fine_of<H>(qk[0], hp, s), 1u);
+        atomicAdd(s_h + fine_of<H>(qk[1], hp, s), 1u);
+      }
+    }
+    for (; i < nv; i += blockDim.x) {
+      uint4 q = __ldcs(p + i);
+      const K* qk = reinterpret_cast<const K*>(&q);
+      atomicAdd(s_h + fine_of<H>(qk[0], hp, s), 1u);
+      atomicAdd(s_h + fine_of<H>(qk[1], hp, s), 1u);
+    }
+    for (uint64_t j = lo + nv * 2 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
+  } else if (sizeof(K) == 4 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
     const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
     const uint64_t nv = (hi - lo) / 4;
     uint64_t i = threadIdx.x;
@@ -403,12 +428,12 @@ constexpr uint32_t kPadMod = 4;
 template <typename K>
 struct PartSmem {
   K raw[TileShape<K>::kTile + 16 / sizeof(K)];              // TMA landing buffer (next tile)
-  K staged[TileShape<K>::kTile + kPadMod * kSub + 2 * kPadMod];  // runs, padded for alignment
-  uint32_t wcnt[kW][kSub];  // per-warp counts -> per-warp slot bases
-  uint32_t toff[kSub + 1];  // tile offsets per bin (unpadded)
-  uint32_t pt[kSub];        // padded staged start per bin
-  uint32_t dst[kSub];       // global write base per bin
-  uint32_t tp[kSub + 1];    // level-2 tile prefix (P2 only)
+  K staged[TileShape<K>::kTile + kPadMod * kMaxBins + 2 * kPadMod];  // runs, padded for alignment
+  uint32_t wcnt[kW][kMaxBins];  // per-warp counts -> per-warp slot bases
+  uint32_t toff[kMaxBins + 1];  // tile offsets per bin (unpadded)
+  uint32_t pt[kMaxBins];        // padded staged start per bin
+  uint32_t dst[kMaxBins];       // global write base per bin
+  uint32_t tp[kMaxBins + 1];    // level-2 tile prefix (P2 only)
   alignas(8) uint64_t bar;  // TMA load barrier
 };
 
@@ -453,7 +478,7 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
 
 // Given s.dst, compute each bin's padded staged start and turn the warp
 // offsets into absolute staged slots.
-__device__ __forceinline__ void pad_bases(uint32_t* pt, uint32_t (*wcnt)[kSub], const uint32_t* toff,
+__device__ __forceinline__ void pad_bases(uint32_t* pt, uint32_t (*wcnt)[kMaxBins], const uint32_t* toff,
                                           const uint32_t* dst, uint32_t nb) {
   if (threadIdx.x < nb) {
     const uint32_t b = threadIdx.x;
@@ -684,10 +709,10 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
   constexpr int VPT = 8192 / kT;  // gathered values per thread (tile <= 8192)
   extern __shared__ __align__(128) unsigned char s_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);
-  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + 16);  // 8192 + 4*kSub + 8
-  uint32_t* toff = staged + 8192 + kPadMod * kSub + 2 * kPadMod;  // kSub + 1
-  uint32_t* base = toff + kSub + 1;                              // kSub
-  uint32_t* tps = base + kSub;                                   // kSub + 1
+  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + 16);  // 8192 + 4*kMaxBins + 8
+  uint32_t* toff = staged + 8192 + kPadMod * kMaxBins + 2 * kPadMod;  // kMaxBins + 1
+  uint32_t* base = toff + kMaxBins + 1;                              // kMaxBins
+  uint32_t* tps = base + kMaxBins;                                   // kMaxBins + 1
   uint64_t lo = 0, hi = 0;
   uint32_t ntiles = 0;
   if (threadIdx.x == 0) {
@@ -1220,7 +1245,7 @@ static size_t probe_smem(int s, int key_bits) {
          (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 + sizeof(BigMap<uint32_t>)
                          : (LocalShape<uint64_t>::kCap + 8) * 8 + sizeof(BigMap<uint64_t>));
 }
-static size_t unpart_smem() { return (8192 + kPadMod * kSub + 2 * kPadMod + 3 * kSub + 4) * 4 + 16; }
+static size_t unpart_smem() { return (8192 + kPadMod * kMaxBins + 2 * kPadMod + 3 * kMaxBins + 4) * 4 + 16; }
 
 size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query) {
   const size_t kb = key_bits / 8;

@@ -49,6 +49,7 @@ struct HashParams {
   uint64_t v;      // hash range (>= 1)
   uint64_t magic;  // fastmod multiplier, valid when mode == kFastmod
   uint64_t mask;   // v - 1, valid when mode == kMask
+  uint64_t magic64;  // floor((2^64 - 1) / v): Barrett reduction of 64-bit mixed values
   uint32_t seed;
   int kind;        // 0 murmur, 1 identity
   int mode;        // kMask / kFastmod / kNone / kGeneric64
@@ -61,6 +62,7 @@ inline HashParams make_hash_params(int kind, uint32_t seed, uint64_t v, int key_
   hp.v = v;
   hp.seed = seed;
   hp.kind = kind;
+  hp.magic64 = UINT64_MAX / v;
   if ((v & (v - 1)) == 0) {
     hp.mode = kMask;
     hp.mask = v - 1;
@@ -98,6 +100,16 @@ __device__ __forceinline__ uint32_t fastmod_u32(uint32_t x, uint64_t magic, uint
   return (uint32_t)__umul64hi(low, (uint64_t)d);
 }
 
+// x mod d for any 64-bit x: q = floor(x * m / 2^64) with m = floor((2^64-1)/d)
+// undershoots floor(x/d) by at most 2, so two conditional subtractions finish.
+__device__ __forceinline__ uint64_t barrett_mod64(uint64_t x, uint64_t m, uint64_t d) {
+  const uint64_t q = __umul64hi(x, m);
+  uint64_t r = x - q * d;
+  if (r >= d) r -= d;
+  if (r >= d) r -= d;
+  return r;
+}
+
 __device__ __forceinline__ uint64_t mix_key(uint32_t key, const HashParams& hp) {
   return hp.kind == HG_KIND_IDENTITY ? (uint64_t)key : (uint64_t)fmix32(key ^ hp.seed);
 }
@@ -116,9 +128,9 @@ __device__ __forceinline__ uint64_t hash_mod(K key, const HashParams& hp) {
       return x;
     case kFastmod:
       if (sizeof(K) == 4) return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
-      return x % hp.v;
+      return barrett_mod64(x, hp.magic64, hp.v);
     default:
-      return x % hp.v;
+      return barrett_mod64(x, hp.magic64, hp.v);
   }
 }
 
@@ -145,7 +157,7 @@ struct Hasher {
     } else if constexpr (MODE == kFastmod && sizeof(K) == 4) {
       return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
     } else {
-      return (uint32_t)(x % hp.v);
+      return (uint32_t)barrett_mod64(x, hp.magic64, hp.v);
     }
   }
 };
