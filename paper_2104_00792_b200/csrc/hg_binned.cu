@@ -495,7 +495,9 @@ template <typename K, int KPT, bool kFull>
 __device__ __forceinline__ void place_tile(PartSmem<K>& s, const K (&kv)[KPT], const uint32_t (&bp)[KPT / 4],
                                            const uint32_t (&rk)[KPT / 2], uint32_t m, uint16_t* __restrict__ pmap) {
   constexpr bool vec = kFull;
+  constexpr int VPL = 16 / sizeof(K);  // consecutive elements per thread in the vector mapping
   const int warp = threadIdx.x >> 5;
+  uint32_t sl[VPL];
 #pragma unroll
   for (int k = 0; k < KPT; k++) {
     const uint32_t e = tile_elem<K>(k, vec);
@@ -503,7 +505,17 @@ __device__ __forceinline__ void place_tile(PartSmem<K>& s, const K (&kv)[KPT], c
       const uint32_t b = (bp[k >> 2] >> ((k & 3) * 8)) & 0xFFu;
       const uint32_t slot = s.wcnt[warp][b] + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
       s.staged[slot] = kv[k];
-      if (pmap) pmap[e] = (uint16_t)slot;
+      if (kFull) {
+        sl[k % VPL] = slot;
+        if (pmap && k % VPL == VPL - 1) {  // VPL consecutive u16 slots -> one store
+          if (VPL == 4)
+            *reinterpret_cast<uint2*>(pmap + e - 3) = make_uint2(sl[0] | (sl[1 % VPL] << 16), sl[2 % VPL] | (sl[3 % VPL] << 16));
+          else
+            *reinterpret_cast<uint32_t*>(pmap + e - 1) = sl[0] | (sl[1 % VPL] << 16);
+        }
+      } else if (pmap) {
+        pmap[e] = (uint16_t)slot;
+      }
     }
   }
   fence_proxy_async();  // staged (generic writes) -> TMA bulk-store reads
@@ -777,18 +789,37 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
     }
     __syncthreads();
     if (threadIdx.x == 0) mbar_arrive(bar);
-    uint32_t pm[VPT];  // position maps load while the runs land
+    if (kLevel == 1 && m == tile && tile == (uint32_t)VPT * kT) {
+      // full level-1 tiles are 16-byte aligned: 8 slots per 16-byte load,
+      // 4 values per 16-byte store
+      uint4 pm[VPT / 8];
+      const uint4* p4 = reinterpret_cast<const uint4*>(pmap + t0);
 #pragma unroll
-    for (int k = 0; k < VPT; k++) {
-      const uint32_t i = k * kT + threadIdx.x;
-      pm[k] = i < m ? pmap[t0 + i] : 0u;
-    }
-    mbar_wait(bar, parity);
-    parity ^= 1;
+      for (int k = 0; k < VPT / 8; k++) pm[k] = p4[k * kT + threadIdx.x];
+      mbar_wait(bar, parity);
+      parity ^= 1;
+      uint4* o4 = reinterpret_cast<uint4*>(out + t0);
 #pragma unroll
-    for (int k = 0; k < VPT; k++) {
-      const uint32_t i = k * kT + threadIdx.x;
-      if (i < m) out[t0 + i] = staged[pm[k]];
+      for (int k = 0; k < VPT / 8; k++) {
+        const uint32_t w[4] = {pm[k].x, pm[k].y, pm[k].z, pm[k].w};
+        const uint32_t c = k * kT + threadIdx.x;
+        o4[2 * c] = make_uint4(staged[w[0] & 0xFFFFu], staged[w[0] >> 16], staged[w[1] & 0xFFFFu], staged[w[1] >> 16]);
+        o4[2 * c + 1] = make_uint4(staged[w[2] & 0xFFFFu], staged[w[2] >> 16], staged[w[3] & 0xFFFFu], staged[w[3] >> 16]);
+      }
+    } else {
+      uint32_t pm[VPT];  // position maps load while the runs land
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t i = k * kT + threadIdx.x;
+        pm[k] = i < m ? pmap[t0 + i] : 0u;
+      }
+      mbar_wait(bar, parity);
+      parity ^= 1;
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t i = k * kT + threadIdx.x;
+        if (i < m) out[t0 + i] = staged[pm[k]];
+      }
     }
     if (kLevel == 1 && threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
   }

@@ -82,5 +82,7 @@ for row in r[2:]:
                  f"{d['launch__registers_per_thread']} | {float(d['smsp__inst_executed.sum']):.3g} |")
 os.makedirs("profiles", exist_ok=True)
 open(f"profiles/{rnd}_ncu_summary.md", "w").write("\n".join(lines) + "\n")
-json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
+old = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}
+old.update(traffic)  # merge: a capture of some kernels keeps the others' figures
+json.dump(old, open("profiles/traffic.json", "w"), indent=1)
 print("\n".join(lines))
