@@ -996,6 +996,17 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
   }
 }
 
+constexpr int kProbeQPT = 16;  // queries per thread per probe batch
+
+template <typename K>
+__device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qhi, K (&qv)[kProbeQPT]) {
+#pragma unroll
+  for (int k = 0; k < kProbeQPT; k++) {
+    const uint32_t j = q0 + k * kT + threadIdx.x;
+    qv[k] = j < qhi ? __ldcs(qpart + j) : K(0);
+  }
+}
+
 // ---- small per-CTA map for deep buckets (high-duplicate inputs)
 constexpr uint32_t kBigDeg = 16;     // buckets deeper than this use the map
 constexpr uint32_t kMapSlots = 256;  // open addressing, power of two
@@ -1078,16 +1089,12 @@ __device__ __forceinline__ void probe_queries(const KeyOf<H>* __restrict__ qpart
                                               const KeyOf<H>* te, const uint32_t* __restrict__ t_off,
                                               const KeyOf<H>* __restrict__ t_edges, uint32_t tlo,
                                               const BigMap<KeyOf<H>>& map, bool overflow, uint32_t* __restrict__ mult_bo,
-                                              uint64_t& matched, uint64_t& total, uint64_t& comps) {
+                                              KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
+                                              uint64_t& comps) {
   using K = typename H::Key;
-  constexpr int QPT = 16;
+  constexpr int QPT = kProbeQPT;
   for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
-    K qv[QPT];
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t j = q0 + k * kT + threadIdx.x;
-      qv[k] = j < qhi ? qpart[j] : K(0);
-    }
+    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);  // the first batch was loaded before staging
     uint32_t m32 = 0, t32 = 0;
     uint64_t c64 = 0;
 #pragma unroll
@@ -1108,13 +1115,13 @@ __device__ __forceinline__ void probe_queries(const KeyOf<H>* __restrict__ qpart
         if (d > kBigDeg && !overflow) {
           c = map_count(map, q);
         } else if (kSmem) {
-          // the first two slots without a branch (buckets hold ~1 key at C = 1)
-          const K e0 = te[a], e1 = te[a + 1];
-          c = (uint32_t)(d > 0 && e0 == q) + (uint32_t)(d > 1 && e1 == q);
-          for (uint32_t t = a + 2; t < e; t += 2) {  // two slots per trip (one may be past e)
-            const K x0 = te[t], x1 = te[t + 1];
-            c += (uint32_t)(x0 == q) + (uint32_t)(t + 1 < e && x1 == q);
-          }
+          // four slots without a branch (at C = 1 over 99% of buckets hold <= 4
+          // keys; the slice buffer is padded so te[a + 3] is always readable),
+          // the rare deeper bucket loops
+          const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
+          c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
+              (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
+          for (uint32_t t = a + 4; t < e; t++) c += (uint32_t)(te[t] == q);
         } else {
           c = 0;
           for (uint32_t t = a; t < e; t++) c += (t_edges[tlo + t] == q);
@@ -1142,10 +1149,11 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
               const uint32_t* __restrict__ q_start, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ mult_bo,
               unsigned long long* __restrict__ agg) {
   using K = typename H::Key;
-  constexpr int QPT = 16;
   constexpr uint32_t VPL = 16 / sizeof(K);
   constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(16) unsigned char s_raw[];
+  __shared__ alignas(8) uint64_t s_bar;
+  __shared__ uint32_t s_deep;
   const uint32_t S = 1u << s;
   uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);                        // S + 1 (+ pad to 8)
   K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 8
@@ -1153,74 +1161,72 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const uint32_t f = blockIdx.x;
   const uint32_t qlo = q_start[f], qhi = q_start[f + 1];
   if (qlo == qhi) return;
+  K qv[kProbeQPT];
+  load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
   const uint32_t tn = thi - tlo;
   const bool in_smem = tn <= kCap;
-  uint32_t sh = 0;
-  __shared__ uint32_t s_deep;
-  if (threadIdx.x == 0) s_deep = in_smem ? 0u : 1u;
-  __syncthreads();
+  // edges: one TMA bulk copy of the 16-byte chunks from the boundary below
+  // tlo (tedges[sh + j] = edge tlo + j) lands while the offsets convert
+  const uint32_t a0 = tlo & ~(VPL - 1);
+  const uint32_t sh = in_smem ? tlo - a0 : 0u;
+  const uint32_t ebytes = in_smem ? ((thi - a0) * (uint32_t)sizeof(K) + 15u) & ~15u : 0u;
+  if (threadIdx.x == 0) {
+    s_deep = in_smem ? 0u : 1u;
+    if (ebytes) {
+      mbar_init(&s_bar, 1);
+      fence_proxy_async();
+      tma_load_1d(tedges, t_edges + a0, ebytes, &s_bar);
+    }
+  }
+  map_clear(map);
   if (in_smem) {
-    // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16 relative to tlo;
-    // also flag the bin if any bucket is deeper than kBigDeg
+    // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16
+    // relative to tlo, three loads in flight per thread; also flag the bin if
+    // any bucket is deeper than kBigDeg
     const uint4* o4 = reinterpret_cast<const uint4*>(t_off + first);
     bool deep = false;
-    for (uint32_t w = threadIdx.x; 4 * w <= nb; w += blockDim.x) {
-      uint4 x;
-      if (4 * w + 3 <= nb) {
-        x = o4[w];
-      } else {
-        uint32_t t[4] = {0, 0, 0, 0};
-        for (uint32_t e = 0; 4 * w + e <= nb; e++) t[e] = t_off[first + 4 * w + e];
-        x = make_uint4(t[0], t[1], t[2], t[3]);
-      }
-      // degrees of buckets 4w..4w+3 (only those below nb exist)
-      const uint32_t i0 = 4 * w;
-      const uint32_t nx = i0 + 4 <= nb ? t_off[first + i0 + 4] : 0u;
-      deep |= (i0 + 1 <= nb && x.y - x.x > kBigDeg) | (i0 + 2 <= nb && x.z - x.y > kBigDeg) |
-              (i0 + 3 <= nb && x.w - x.z > kBigDeg) | (i0 + 4 <= nb && nx - x.w > kBigDeg);
-      const uint32_t lo2 = ((x.x - tlo) & 0xFFFFu) | ((x.y - tlo) << 16);
-      const uint32_t hi2 = ((x.z - tlo) & 0xFFFFu) | ((x.w - tlo) << 16);
-      reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
-    }
-    if (__any_sync(0xffffffffu, deep) && (threadIdx.x & 31) == 0) s_deep = 1u;
-    // edges: 16-byte chunks from the boundary below tlo; tedges[sh + j] = edge tlo + j
-    const uint32_t a0 = tlo & ~(VPL - 1);
-    sh = tlo - a0;
-    const uint32_t nch = (thi - a0 + VPL - 1) / VPL;
-    const uint4* e4 = reinterpret_cast<const uint4*>(t_edges + a0);
-    uint4* d4 = reinterpret_cast<uint4*>(tedges);
-    for (uint32_t c0 = 0; c0 < nch; c0 += 4 * kT) {
-      uint4 x[4];
+    constexpr int R = 3;
+    for (uint32_t w0 = threadIdx.x; 4 * w0 <= nb; w0 += R * blockDim.x) {
+      uint4 x[R];
+      uint32_t nx[R];
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const uint32_t c = c0 + k * kT + threadIdx.x;
-        if (c < nch) {
-          if ((c + 1) * VPL + a0 <= thi) {
-            x[k] = e4[c];
-          } else {  // last chunk: do not read past the edge array
-            K t[VPL];
-            for (uint32_t e = 0; e < VPL; e++) t[e] = a0 + c * VPL + e < thi ? t_edges[a0 + c * VPL + e] : K(0);
-            x[k] = *reinterpret_cast<uint4*>(t);
-          }
+      for (int r = 0; r < R; r++) {
+        const uint32_t w = w0 + r * blockDim.x, i0 = 4 * w;
+        x[r] = make_uint4(0, 0, 0, 0);
+        nx[r] = 0;
+        if (i0 + 4 <= nb) {
+          x[r] = o4[w];
+          nx[r] = t_off[first + i0 + 4];
+        } else if (i0 <= nb) {
+          uint32_t t[4] = {0, 0, 0, 0};
+          for (uint32_t e = 0; i0 + e <= nb; e++) t[e] = t_off[first + i0 + e];
+          x[r] = make_uint4(t[0], t[1], t[2], t[3]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const uint32_t c = c0 + k * kT + threadIdx.x;
-        if (c < nch) d4[c] = x[k];
+      for (int r = 0; r < R; r++) {
+        const uint32_t w = w0 + r * blockDim.x, i0 = 4 * w;
+        if (i0 > nb) break;
+        // degrees of buckets i0..i0+3 (only those below nb exist)
+        deep |= (i0 + 1 <= nb && x[r].y - x[r].x > kBigDeg) | (i0 + 2 <= nb && x[r].z - x[r].y > kBigDeg) |
+                (i0 + 3 <= nb && x[r].w - x[r].z > kBigDeg) | (i0 + 4 <= nb && nx[r] - x[r].w > kBigDeg);
+        const uint32_t lo2 = ((x[r].x - tlo) & 0xFFFFu) | ((x[r].y - tlo) << 16);
+        const uint32_t hi2 = ((x[r].z - tlo) & 0xFFFFu) | ((x[r].w - tlo) << 16);
+        reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
       }
     }
+    __syncthreads();  // s_deep initialised
+    if (__any_sync(0xffffffffu, deep) && (threadIdx.x & 31) == 0) s_deep = 1u;
+    if (threadIdx.x == 0 && ebytes) mbar_wait(&s_bar, 0);
   }
   __syncthreads();
   const K* te = tedges + sh;
   // Buckets deeper than kBigDeg (high-duplicate inputs) are answered from a
   // small smem map key -> occurrences, built once per bin, instead of an
-  // O(degree) scan per query.
-  map_clear(map);
-  __syncthreads();
+  // O(degree) scan per query (the map was cleared before staging).
   if (s_deep) {
     // each warp scans 32 consecutive buckets per round and feeds the deep
     // ones (ballot) to the map cooperatively
@@ -1256,10 +1262,10 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   uint64_t matched = 0, total = 0, comps = 0;
   if (in_smem)
     probe_queries<H, true>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow, mult_bo,
-                           matched, total, comps);
+                           qv, matched, total, comps);
   else
     probe_queries<H, false>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow,
-                            mult_bo, matched, total, comps);
+                            mult_bo, qv, matched, total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
 }
 
