@@ -827,96 +827,219 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
 
 // --------------------------------------------------------------------------- C: local build
 
-// One CTA per fine bin (two CTAs per SM): the bin's keys arrive with 128-bit
-// loads into registers, packed-u16 smem counters rank them (one atomic per
-// key per pass), and offsets (4 per store) and edges (128-bit stores) leave
-// as aligned coalesced streams.  `src` may alias `edges`: every load of a CTA
-// precedes its first barrier and it only writes inside its own range.
+// Exclusive scan of the nb packed-u16 bucket counters of a 1024-thread CTA
+// (8 consecutive words = 16 buckets per thread, nb <= 16384), in place, and
+// the bin's offsets (lo + start) written 16 per thread as 16-byte stores.
+__device__ __forceinline__ void scan_c16_offsets(uint32_t* c16, uint32_t nb, uint32_t lo, uint32_t* __restrict__ off) {
+  __shared__ uint32_t s_w[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nwords = (nb + 1) / 2;
+  const uint32_t w0 = threadIdx.x * 8;
+  uint32_t x[8];
+  if (w0 + 8 <= nwords) {
+    const uint4 a = reinterpret_cast<const uint4*>(c16)[2 * threadIdx.x];
+    const uint4 b = reinterpret_cast<const uint4*>(c16)[2 * threadIdx.x + 1];
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = w0 + k < nwords ? c16[w0 + k] : 0u;
+  }
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) sum += (x[k] & 0xFFFFu) + (x[k] >> 16);
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = s_w[lane];
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    s_w[lane] = ti - t;
+  }
+  __syncthreads();
+  uint32_t run = s_w[warp] + inc - sum;
+  uint32_t o[16];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const uint32_t p0 = run, p1 = run + (x[k] & 0xFFFFu);
+    run = p1 + (x[k] >> 16);
+    x[k] = (p0 & 0xFFFFu) | (p1 << 16);
+    o[2 * k] = lo + p0;
+    o[2 * k + 1] = lo + p1;
+  }
+  if (w0 + 8 <= nwords) {
+    reinterpret_cast<uint4*>(c16)[2 * threadIdx.x] = make_uint4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<uint4*>(c16)[2 * threadIdx.x + 1] = make_uint4(x[4], x[5], x[6], x[7]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      if (w0 + k < nwords) c16[w0 + k] = x[k];
+  }
+  const uint32_t b0 = threadIdx.x * 16;
+  if (b0 + 16 <= nb) {
+    uint4* o4 = reinterpret_cast<uint4*>(off + b0);
+#pragma unroll
+    for (int k = 0; k < 4; k++) o4[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+      if (b0 + k < nb) off[b0 + k] = o[k];
+  }
+  __syncthreads();
+}
+
+template <typename K>
+struct LocalPShape {
+  static constexpr int kThreads = 1024;
+  static constexpr int kVPL = 16 / sizeof(K);
+  static constexpr uint32_t kCap = LocalShape<K>::kCap;                      // keys per bin in smem
+  static constexpr uint32_t kChunks = (kCap + 2 * kVPL - 2) / kVPL;          // 16-byte chunks a bin spans
+  static constexpr int kCPT = (kChunks + kThreads - 1) / kThreads;           // chunks per thread
+  static constexpr uint32_t kElems = kChunks * kVPL;
+  __host__ __device__ static size_t c16_bytes(int s) { return (((size_t)1 << s) / 2 * 4 + 127) & ~(size_t)127; }
+  static size_t smem(int s) { return c16_bytes(s) + 2 * (size_t)kChunks * 16; }
+};
+
 template <typename H>
-__global__ void __launch_bounds__(kT, 2)
-k_local_build(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
-              uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
+__global__ void __launch_bounds__(1024, 1)
+k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
+                uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
   using K = typename H::Key;
-  constexpr int VPL = 16 / sizeof(K);                       // keys per 16-byte chunk
-  constexpr int NCH = (LocalShape<K>::kKPT + VPL - 1) / VPL + 1;  // chunks per thread
-  constexpr uint32_t kCap = LocalShape<K>::kCap;
-  extern __shared__ __align__(16) unsigned char s_raw[];
+  using PS = LocalPShape<K>;
+  constexpr int NT = PS::kThreads;
+  constexpr uint32_t VPL = PS::kVPL;
+  constexpr int CPT = PS::kCPT;
+  constexpr uint32_t kCap = PS::kCap;
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  __shared__ alignas(8) uint64_t s_bar;
   const uint32_t S = 1u << s;
-  uint32_t* c16 = reinterpret_cast<uint32_t*>(s_raw);  // S/2 words
-  K* staged = reinterpret_cast<K*>(s_raw + (S / 2) * 4);  // kCap + VPL keys, chunk-aligned to global
-  const uint32_t f = blockIdx.x;
-  const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
-  const uint32_t cnt = hi - lo;
-  const uint64_t first = (uint64_t)f << s;
-  const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
-  if (f == nfine - 1 && threadIdx.x == 0) offsets[v] = hi;
-  if (cnt > kCap) return;  // k_local_build_big
-  const uint32_t lo_al = lo & ~(uint32_t)(VPL - 1);
-  const uint32_t nch = (hi - lo_al + VPL - 1) / VPL;
-  const uint4* src4 = reinterpret_cast<const uint4*>(src + lo_al);
-  K kv[NCH * VPL];
-#pragma unroll
-  for (int i = 0; i < NCH; i++) {
-    const uint32_t c = i * kT + threadIdx.x;
-    uint4 q = make_uint4(0, 0, 0, 0);
-    if (c < nch) q = src4[c];
-    const K* qk = reinterpret_cast<const K*>(&q);
-#pragma unroll
-    for (int j = 0; j < VPL; j++) kv[i * VPL + j] = qk[j];
-  }
-  for (uint32_t i = threadIdx.x; i < (nb + 1) / 2; i += blockDim.x) c16[i] = 0;
-  __syncthreads();
-  auto valid = [&](int i, int j) {
-    const uint32_t g = lo_al + (i * kT + threadIdx.x) * VPL + j;
-    return (i * kT + threadIdx.x) < nch && g >= lo && g < hi;
+  uint32_t* c16 = reinterpret_cast<uint32_t*>(s_raw);                 // S/2 words of packed u16 counters
+  K* raw = reinterpret_cast<K*>(s_raw + PS::c16_bytes(s));            // next bin's keys (TMA)
+  K* staged = raw + PS::kElems;                                       // this bin's edges, chunk-aligned to global
+  if (blockIdx.x == 0 && threadIdx.x == 0) offsets[v] = fine_start[nfine];
+  auto next_small = [&](uint32_t f) -> uint32_t {  // bins above kCap belong to k_local_build_big
+    while (f < nfine && fine_start[f + 1] - fine_start[f] > kCap) f += gridDim.x;
+    return f;
   };
-#pragma unroll
-  for (int i = 0; i < NCH; i++)
-#pragma unroll
-    for (int j = 0; j < VPL; j++)
-      if (valid(i, j)) {
-        const uint32_t l = H::bucket(kv[i * VPL + j], hp) - (uint32_t)first;
-        atomicAdd(c16 + (l >> 1), 1u << ((l & 1) * 16));
-      }
-  __syncthreads();
-  block_exscan_u16(c16, nb);
-  // offsets: word pair (2 words = 4 values) per thread -> one 16-byte store
-  for (uint32_t w = threadIdx.x; 4 * w < nb; w += blockDim.x) {
-    const uint32_t a = c16[2 * w], b = (2 * w + 1) * 2 < nb + 1 ? c16[2 * w + 1] : 0u;
-    const uint4 o = make_uint4(lo + (a & 0xFFFFu), lo + (a >> 16), lo + (b & 0xFFFFu), lo + (b >> 16));
-    if (4 * w + 3 < nb) {
-      *reinterpret_cast<uint4*>(offsets + first + 4 * w) = o;
-    } else {
-      const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
-      for (uint32_t e = 0; 4 * w + e < nb; e++) offsets[first + 4 * w + e] = ov[e];
+  // bin f's keys [lo, hi) land at raw[lo - lo_al ...]: the 16-byte aligned
+  // part by TMA (thread 0), the < VPL keys after the last boundary by threads
+  // 0..VPL-1 (nothing past hi is read)
+  auto fetch = [&](uint32_t f) {
+    const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
+    const uint32_t lo_al = lo & ~(VPL - 1), hi_al = hi & ~(VPL - 1);
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = hi_al > lo_al ? (hi_al - lo_al) * (uint32_t)sizeof(K) : 0u;
+      if (bytes) tma_load_1d(raw, src + lo_al, bytes, &s_bar);
+      else mbar_arrive(&s_bar);
     }
+    if (threadIdx.x < VPL) {
+      const uint32_t g = hi_al + threadIdx.x;
+      if (g >= lo && g < hi) raw[g - lo_al] = src[g];
+    }
+  };
+  uint32_t f = next_small(blockIdx.x);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_proxy_async();
   }
   __syncthreads();
-  const uint32_t sh = lo - lo_al;
+  if (f < nfine) fetch(f);
+  uint32_t parity = 0;
+  while (f < nfine) {
+    const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
+    const uint32_t cnt = hi - lo;
+    const uint32_t lo_al = lo & ~(VPL - 1), sh = lo - lo_al;
+    const uint32_t nch = (sh + cnt + VPL - 1) / VPL;
+    const uint64_t first = (uint64_t)f << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
+    const uint32_t fn = next_small(f + gridDim.x);
+    mbar_wait(&s_bar, parity);
+    parity ^= 1;
+    __syncthreads();  // the tail keys written by threads 0..VPL-1 are visible
+    K kv[CPT * VPL];
+    const uint4* raw4 = reinterpret_cast<const uint4*>(raw);
 #pragma unroll
-  for (int i = 0; i < NCH; i++)
+    for (int i = 0; i < CPT; i++) {
+      const uint32_t c = i * NT + threadIdx.x;
+      uint4 q = make_uint4(0, 0, 0, 0);
+      if (c < nch) q = raw4[c];
+      const K* qk = reinterpret_cast<const K*>(&q);
 #pragma unroll
-    for (int j = 0; j < VPL; j++)
-      if (valid(i, j)) {
-        const K key = kv[i * VPL + j];
-        const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
-        const uint32_t sft = (l & 1) * 16;
-        const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sft);
-        staged[sh + ((old >> sft) & 0xFFFFu)] = key;
-      }
-  __syncthreads();
-  // edges: chunk c covers global [lo_al + c*VPL, +VPL) == staged[c*VPL, +VPL)
-  uint4* dst4 = reinterpret_cast<uint4*>(edges + lo_al);
-  const uint4* stg4 = reinterpret_cast<const uint4*>(staged);
-  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
-    const uint32_t g0 = lo_al + c * VPL;
-    if (g0 >= lo && g0 + VPL <= hi) {
-      dst4[c] = stg4[c];
-    } else {
-      for (int j = 0; j < VPL; j++)
-        if (g0 + j >= lo && g0 + j < hi) edges[g0 + j] = staged[c * VPL + j];
+      for (int j = 0; j < (int)VPL; j++) kv[i * VPL + j] = qk[j];
     }
+    for (uint32_t i = threadIdx.x; i < (nb + 1) / 2; i += NT) c16[i] = 0;
+    __syncthreads();  // raw consumed, counters zero
+    if (fn < nfine) fetch(fn);
+    // count: the atomic's old value is the key's rank inside its bucket.
+    // Only the first and last chunk of a bin can be partial, so validity is
+    // decided per chunk and full chunks run branch-free.
+    uint32_t pk[CPT * VPL];
+    auto count_key = [&](K key) -> uint32_t {
+      const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
+      const uint32_t sft = (l & 1) * 16;
+      const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sft);
+      return (l << 16) | ((old >> sft) & 0xFFFFu);
+    };
+#pragma unroll
+    for (int i = 0; i < CPT; i++) {
+      const uint32_t c = i * NT + threadIdx.x;
+      const uint32_t e0 = c * VPL;
+#pragma unroll
+      for (int j = 0; j < (int)VPL; j++) pk[i * VPL + j] = 0xFFFFFFFFu;
+      if (c < nch) {
+        if (e0 >= sh && e0 + VPL <= sh + cnt) {
+#pragma unroll
+          for (int j = 0; j < (int)VPL; j++) pk[i * VPL + j] = count_key(kv[i * VPL + j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < (int)VPL; j++)
+            if (e0 + j - sh < cnt) pk[i * VPL + j] = count_key(kv[i * VPL + j]);
+        }
+      }
+    }
+    __syncthreads();
+    scan_c16_offsets(c16, nb, lo, offsets + first);
+    if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
+    __syncthreads();
+    K* stg = staged + sh;
+#pragma unroll
+    for (int i = 0; i < CPT; i++) {
+      const uint32_t c = i * NT + threadIdx.x;
+      if (c < nch) {
+#pragma unroll
+        for (int j = 0; j < (int)VPL; j++) {
+          const uint32_t p = pk[i * VPL + j];
+          if (p != 0xFFFFFFFFu) stg[get16(c16, p >> 16) + (p & 0xFFFFu)] = kv[i * VPL + j];
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    // edges: aligned body by one bulk store, head and tail (< VPL each) by threads
+    const uint32_t g0 = min(hi, (lo + VPL - 1) & ~(VPL - 1));
+    const uint32_t g1 = max(g0, hi & ~(VPL - 1));
+    if (threadIdx.x == 0 && g1 > g0) {
+      tma_store_1d(edges + g0, staged + (g0 - lo_al), (g1 - g0) * (uint32_t)sizeof(K));
+      tma_store_commit();
+    }
+    if (threadIdx.x < VPL) {
+      const uint32_t gh = lo + threadIdx.x;
+      if (gh < g0) edges[gh] = staged[gh - lo_al];
+      const uint32_t gt = g1 + threadIdx.x;
+      if (gt < hi) edges[gt] = staged[gt - lo_al];
+    }
+    f = fn;
   }
+  if (threadIdx.x == 0) tma_store_wait_all();
 }
 
 // Fine bins above the smem capacity (high-duplicate inputs): the bin's keys
@@ -1151,7 +1274,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   using K = typename H::Key;
   constexpr uint32_t VPL = 16 / sizeof(K);
   constexpr uint32_t kCap = LocalShape<K>::kCap;
-  extern __shared__ __align__(16) unsigned char s_raw[];
+  extern __shared__ __align__(128) unsigned char s_raw[];
   __shared__ alignas(8) uint64_t s_bar;
   __shared__ uint32_t s_deep;
   const uint32_t S = 1u << s;
@@ -1274,9 +1397,6 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
 static size_t part_smem(int key_bits) {
   return key_bits == 32 ? sizeof(PartSmem<uint32_t>) : sizeof(PartSmem<uint64_t>);
 }
-static size_t local_smem(int s, int key_bits) {
-  return (size_t)(1u << s) / 2 * 4 + (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 : (LocalShape<uint64_t>::kCap + 4) * 8);
-}
 static size_t probe_smem(int s, int key_bits) {
   return (size_t)((2 * ((1u << s) + 8) + 15) & ~15u) +
          (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 + sizeof(BigMap<uint32_t>)
@@ -1393,11 +1513,11 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   if (rc) return rc;
   uint32_t* scratch = ws.take<uint32_t>((size_t)num_sms() * (1u << L.s));
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
-  const size_t smC = local_smem(L.s, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
   const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
-  HG_LAUNCH("hg_local_build", k_local_build<H>, L.nfine, kT, smC, st, grouped, po.fine_start, L.nfine, hp, L.s, v,
-            offsets, edges);
+  const size_t smC = LocalPShape<K>::smem(L.s);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+  HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
+            L.nfine, hp, L.s, v, offsets, edges);
   // oversized fine bins: with two levels their keys sit in edges (in place), so
   // they are copied to the free level-1 buffer first
   const int copy = L.two_level ? 1 : 0;
