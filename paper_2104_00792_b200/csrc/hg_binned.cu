@@ -1194,7 +1194,7 @@ __device__ __forceinline__ void map_add(BigMap<K>& m, K key, bool ok) {
 }
 
 template <typename K>
-__device__ __forceinline__ uint32_t map_count(const BigMap<K>& m, K key) {
+__device__ __noinline__ uint32_t map_count(const BigMap<K>& m, K key) {
   uint32_t i = map_slot(key);
   for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
     if (m.state[i] == 0) return 0;
@@ -1203,61 +1203,101 @@ __device__ __forceinline__ uint32_t map_count(const BigMap<K>& m, K key) {
   return 0;
 }
 
-// The bin's queries, 16 per thread per batch (loads first), each answered by
-// IntersectArray over its bucket (kSmem: the staged slice; else global
-// memory) or by the deep-bucket map.
-template <typename H, bool kSmem>
-__device__ __forceinline__ void probe_queries(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
-                                              const HashParams& hp, uint32_t first, const uint16_t* off16,
-                                              const KeyOf<H>* te, const uint32_t* __restrict__ t_off,
-                                              const KeyOf<H>* __restrict__ t_edges, uint32_t tlo,
-                                              const BigMap<KeyOf<H>>& map, bool overflow, uint32_t* __restrict__ mult_bo,
-                                              KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
-                                              uint64_t& comps) {
+// Slices above the smem capacity: the bin's queries, 16 per thread per batch,
+// each answered by IntersectArray over its bucket in global memory or by the
+// deep-bucket map.
+template <typename H>
+__device__ __forceinline__ void probe_queries_global(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
+                                                     const HashParams& hp, const uint32_t* __restrict__ t_off,
+                                                     const KeyOf<H>* __restrict__ t_edges, const BigMap<KeyOf<H>>& map,
+                                                     bool overflow, uint32_t* __restrict__ mult_bo,
+                                                     KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
+                                                     uint64_t& comps) {
   using K = typename H::Key;
   constexpr int QPT = kProbeQPT;
   for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
-    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);  // the first batch was loaded before staging
-    uint32_t m32 = 0, t32 = 0;
-    uint64_t c64 = 0;
+    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);
 #pragma unroll
     for (int k = 0; k < QPT; k++) {
       const uint32_t j = q0 + k * kT + threadIdx.x;
       if (j < qhi) {
         const K q = qv[k];
         const uint32_t h = H::bucket(q, hp);
-        uint32_t a, e, c;
-        if (kSmem) {
-          a = off16[h - first];
-          e = off16[h - first + 1];
-        } else {
-          a = t_off[h] - tlo;
-          e = t_off[h + 1] - tlo;
-        }
-        const uint32_t d = e - a;
-        if (d > kBigDeg && !overflow) {
-          c = map_count(map, q);
-        } else if (kSmem) {
-          // four slots without a branch (at C = 1 over 99% of buckets hold <= 4
-          // keys; the slice buffer is padded so te[a + 3] is always readable),
-          // the rare deeper bucket loops
-          const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
-          c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
-              (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
-          for (uint32_t t = a + 4; t < e; t++) c += (uint32_t)(te[t] == q);
-        } else {
-          c = 0;
-          for (uint32_t t = a; t < e; t++) c += (t_edges[tlo + t] == q);
-        }
+        const uint32_t a = t_off[h], e = t_off[h + 1];
+        uint32_t c = 0;
+        if (e - a > kBigDeg && !overflow) c = map_count(map, q);
+        else
+          for (uint32_t t = a; t < e; t++) c += (t_edges[t] == q);
+        mult_bo[j] = c;
+        matched += (c != 0);
+        total += c;
+        comps += e - a;
+      }
+    }
+  }
+}
+
+// The bin's queries against the staged slice, 16 per thread per batch (the
+// loads were issued first), in phases so the hashes, offset loads and slot
+// loads of all 16 queries overlap: (1) hash + both u16 offsets, packed; (2)
+// IntersectArray count over the bucket.  Four slots run without a branch (the
+// slice buffer is padded so te[a + 3] is always readable); queries are
+// size-biased towards deep buckets (~9% see more than four keys at C = 1, i.e.
+// almost every warp), so the rest runs as a warp-uniform loop to the warp's
+// deepest bucket rather than a divergent per-lane loop.  Buckets deeper than
+// kBigDeg are answered from the map (one warp-uniform check per batch).
+template <typename H>
+__device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
+                                                   const HashParams& hp, uint32_t first, const uint16_t* off16,
+                                                   const KeyOf<H>* te, const BigMap<KeyOf<H>>& map, bool overflow,
+                                                   uint32_t* __restrict__ mult_bo, KeyOf<H> (&qv)[kProbeQPT],
+                                                   uint64_t& matched, uint64_t& total, uint64_t& comps) {
+  using K = typename H::Key;
+  constexpr int QPT = kProbeQPT;
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
+    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);  // the first batch was loaded before staging
+    const uint32_t kmax = (qhi - q0 + kT - 1) / kT;       // query slots this batch fills (CTA-uniform)
+    uint32_t ae[QPT];
+    bool deep = false;
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      ae[k] = 0;
+      if ((uint32_t)k >= kmax) continue;
+      if (q0 + k * kT + threadIdx.x < qhi) {
+        const uint32_t l = H::bucket(qv[k], hp) - first;
+        ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
+        deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
+      }
+    }
+    const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
+    uint32_t m32 = 0, t32 = 0, d32 = 0;
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      if ((uint32_t)k >= kmax) break;
+      const K q = qv[k];
+      const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
+      const bool mapped = use_map && d > kBigDeg;
+      const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
+      uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
+                   (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
+      const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped ? 0u : d);
+      for (uint32_t t = 4; t < dmax; t++) {
+        const bool in = t < d;
+        const K x = in ? te[a + t] : K(0);
+        c += (uint32_t)(in & (x == q));
+      }
+      if (use_map && mapped) c = map_count(map, q);
+      const uint32_t j = q0 + k * kT + threadIdx.x;
+      if (j < qhi) {
         mult_bo[j] = c;
         m32 += (c != 0);
         t32 += c;
-        c64 += d;
+        d32 += d;
       }
     }
     matched += m32;
     total += t32;
-    comps += c64;
+    comps += d32;
   }
 }
 
@@ -1384,11 +1424,10 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const bool overflow = map.full != 0;
   uint64_t matched = 0, total = 0, comps = 0;
   if (in_smem)
-    probe_queries<H, true>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow, mult_bo,
-                           qv, matched, total, comps);
+    probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, mult_bo, qv, matched, total,
+                          comps);
   else
-    probe_queries<H, false>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, t_off, t_edges, tlo, map, overflow,
-                            mult_bo, qv, matched, total, comps);
+    probe_queries_global<H>(qpart, qlo, qhi, hp, t_off, t_edges, map, overflow, mult_bo, qv, matched, total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
 }
 
