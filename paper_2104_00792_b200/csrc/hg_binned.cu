@@ -712,47 +712,52 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
 // from the level-2 tile table, run bases from meta; level 1: each CTA replays
 // its chunk's tiles with cursors from the column-scanned counts.  Each run is
 // pulled back into its padded staged slot range (TMA for the aligned body),
-// then out[i] = staged[pmap[i]].
+// then out[i] = staged[pmap[i]].  Two staging buffers: tile i+1's runs are in
+// flight (meta read, bulk loads issued) while tile i is gathered.
+constexpr uint32_t kUnpStaged = 8192 + kPadMod * kMaxBins + 2 * kPadMod;
+
 template <int kLevel>
 __global__ void __launch_bounds__(kT, 2)
 k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
          const uint32_t* __restrict__ meta, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
          const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
   constexpr int VPT = 8192 / kT;  // gathered values per thread (tile <= 8192)
+  constexpr uint32_t TO = kMaxBins + 1;
   extern __shared__ __align__(128) unsigned char s_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);
-  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + 16);  // 8192 + 4*kMaxBins + 8
-  uint32_t* toff = staged + 8192 + kPadMod * kMaxBins + 2 * kPadMod;  // kMaxBins + 1
-  uint32_t* base = toff + kMaxBins + 1;                              // kMaxBins
-  uint32_t* tps = base + kMaxBins;                                   // kMaxBins + 1
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_raw);                 // 2
+  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw + 16);         // 2 x kUnpStaged
+  uint32_t* toff = staged + 2 * kUnpStaged;                           // 2 x (kMaxBins + 1)
+  uint32_t* base = toff + 2 * TO;                                     // 2 x kMaxBins
+  uint32_t* tps = base + 2 * kMaxBins;                                // kMaxBins + 1
+  const uint32_t nbb = kLevel == 1 ? nb : kSub;
   uint64_t lo = 0, hi = 0;
   uint32_t ntiles = 0;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_proxy_async();
   }
   if (kLevel == 1) {
     lo = (uint64_t)blockIdx.x * chunk;
     hi = min(n, lo + chunk);
-    if (threadIdx.x < nb) base[threadIdx.x] = c_start[threadIdx.x] + M[(uint64_t)blockIdx.x * nb + threadIdx.x];
+    ntiles = hi > lo ? (uint32_t)((hi - lo + tile - 1) / tile) : 0u;
   } else {
     for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) tps[i] = tp_g[i];
   }
   __syncthreads();
-  if (kLevel == 2) ntiles = tps[nb];
-  const uint32_t nbb = kLevel == 1 ? nb : kSub;
-  uint32_t parity = 0;
-  for (uint64_t it = (kLevel == 1 ? lo : blockIdx.x);; it += (kLevel == 1 ? tile : gridDim.x)) {
-    uint32_t m;
-    uint64_t t0, tix;
+  if (kLevel == 2) {
+    const uint32_t tot = tps[nb];
+    ntiles = tot > blockIdx.x ? (tot - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+  }
+  if (ntiles == 0) return;
+  // this CTA's i-th tile: first element, size, index into meta
+  auto tile_of = [&](uint32_t i, uint64_t& t0, uint32_t& m, uint64_t& tix) {
     if (kLevel == 1) {
-      if (it >= hi) break;
-      t0 = it;
-      m = (uint32_t)min((uint64_t)tile, hi - it);
-      tix = it / tile;
+      t0 = lo + (uint64_t)i * tile;
+      m = (uint32_t)min((uint64_t)tile, hi - t0);
+      tix = t0 / tile;
     } else {
-      if (it >= ntiles) break;
-      const uint32_t t = (uint32_t)it;
+      const uint32_t t = blockIdx.x + i * gridDim.x;
       uint32_t a = 0, z = nb;
       while (z - a > 1) {
         const uint32_t mid = (a + z) >> 1;
@@ -762,66 +767,98 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       m = min(tile, c_start[a + 1] - (uint32_t)t0);
       tix = t;
     }
-    fence_proxy_async();
-    __syncthreads();  // previous gather done: staged is free
+  };
+  // run offsets + global bases of tile i into buffer bf; level-1 bases chain
+  // from the previous tile (buffer bf ^ 1)
+  auto load_meta = [&](uint32_t i, int bf) {
+    uint64_t t0, tix;
+    uint32_t m;
+    tile_of(i, t0, m, tix);
     if (kLevel == 1) {
-      for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) toff[i] = meta[tix * (nb + 1) + i];
+      for (uint32_t x = threadIdx.x; x <= nb; x += blockDim.x) toff[bf * TO + x] = meta[tix * (nb + 1) + x];
+      if (threadIdx.x < nb) {
+        const uint32_t b = threadIdx.x, pb = (bf ^ 1) * TO;
+        base[bf * kMaxBins + b] = i == 0 ? c_start[b] + M[(uint64_t)blockIdx.x * nb + b]
+                                         : base[(bf ^ 1) * kMaxBins + b] + toff[pb + b + 1] - toff[pb + b];
+      }
     } else {
-      for (uint32_t i = threadIdx.x; i < kSub; i += blockDim.x) base[i] = meta[tix * (2 * kSub + 1) + i];
-      for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) toff[i] = meta[tix * (2 * kSub + 1) + kSub + i];
+      for (uint32_t x = threadIdx.x; x < kSub; x += blockDim.x) base[bf * kMaxBins + x] = meta[tix * (2 * kSub + 1) + x];
+      for (uint32_t x = threadIdx.x; x <= kSub; x += blockDim.x)
+        toff[bf * TO + x] = meta[tix * (2 * kSub + 1) + kSub + x];
     }
-    __syncthreads();
+  };
+  // one thread per bin: aligned body by TMA, < 4-element head/tail by hand
+  auto issue = [&](int bf) {
     if (threadIdx.x < nbb) {
       const uint32_t b = threadIdx.x;
-      const uint32_t cnt = toff[b + 1] - toff[b];
+      const uint32_t cnt = toff[bf * TO + b + 1] - toff[bf * TO + b];
       if (cnt) {
-        const uint32_t g = base[b];
-        const uint32_t p = pad_start(toff[b], b, g);
+        uint32_t* st = staged + bf * kUnpStaged;
+        const uint32_t g = base[bf * kMaxBins + b];
+        const uint32_t p = pad_start(toff[bf * TO + b], b, g);
         const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
         const uint32_t body = (cnt - h) & ~(kPadMod - 1);
         if (body) {
-          mbar_expect_tx(bar, body * 4);
-          tma_load_1d_tx(staged + p + h, vals + g + h, body * 4, bar);
+          mbar_expect_tx(bar + bf, body * 4);
+          tma_load_1d_tx(st + p + h, vals + g + h, body * 4, bar + bf);
         }
-        for (uint32_t i = 0; i < h; i++) staged[p + i] = vals[g + i];
-        for (uint32_t i = h + body; i < cnt; i++) staged[p + i] = vals[g + i];
+        for (uint32_t i = 0; i < h; i++) st[p + i] = vals[g + i];
+        for (uint32_t i = h + body; i < cnt; i++) st[p + i] = vals[g + i];
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) mbar_arrive(bar);
-    if (kLevel == 1 && m == tile && tile == (uint32_t)VPT * kT) {
-      // full level-1 tiles are 16-byte aligned: 8 slots per 16-byte load,
-      // 4 values per 16-byte store
-      uint4 pm[VPT / 8];
+  };
+  load_meta(0, 0);
+  __syncthreads();
+  issue(0);
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(bar);
+  for (uint32_t it = 0; it < ntiles; it++) {
+    const int cur = it & 1, nxt = cur ^ 1;
+    const bool more = it + 1 < ntiles;
+    uint64_t t0, tix;
+    uint32_t m;
+    tile_of(it, t0, m, tix);
+    const uint32_t* st = staged + cur * kUnpStaged;
+    const bool vec = kLevel == 1 && m == tile && tile == (uint32_t)VPT * kT;
+    // position maps of tile it load while tile it+1's runs are requested
+    uint4 pm4[VPT / 8];
+    uint32_t pm[VPT];
+    if (vec) {
       const uint4* p4 = reinterpret_cast<const uint4*>(pmap + t0);
 #pragma unroll
-      for (int k = 0; k < VPT / 8; k++) pm[k] = p4[k * kT + threadIdx.x];
-      mbar_wait(bar, parity);
-      parity ^= 1;
-      uint4* o4 = reinterpret_cast<uint4*>(out + t0);
-#pragma unroll
-      for (int k = 0; k < VPT / 8; k++) {
-        const uint32_t w[4] = {pm[k].x, pm[k].y, pm[k].z, pm[k].w};
-        const uint32_t c = k * kT + threadIdx.x;
-        o4[2 * c] = make_uint4(staged[w[0] & 0xFFFFu], staged[w[0] >> 16], staged[w[1] & 0xFFFFu], staged[w[1] >> 16]);
-        o4[2 * c + 1] = make_uint4(staged[w[2] & 0xFFFFu], staged[w[2] >> 16], staged[w[3] & 0xFFFFu], staged[w[3] >> 16]);
-      }
+      for (int k = 0; k < VPT / 8; k++) pm4[k] = p4[k * kT + threadIdx.x];
     } else {
-      uint32_t pm[VPT];  // position maps load while the runs land
 #pragma unroll
       for (int k = 0; k < VPT; k++) {
         const uint32_t i = k * kT + threadIdx.x;
         pm[k] = i < m ? pmap[t0 + i] : 0u;
       }
-      mbar_wait(bar, parity);
-      parity ^= 1;
+    }
+    if (more) load_meta(it + 1, nxt);
+    __syncthreads();
+    if (more) issue(nxt);
+    mbar_wait(bar + cur, (it >> 1) & 1);
+    if (vec) {
+      // full level-1 tiles are 16-byte aligned: 8 slots per 16-byte load,
+      // 4 values per 16-byte store
+      uint4* o4 = reinterpret_cast<uint4*>(out + t0);
+#pragma unroll
+      for (int k = 0; k < VPT / 8; k++) {
+        const uint32_t w[4] = {pm4[k].x, pm4[k].y, pm4[k].z, pm4[k].w};
+        const uint32_t c = k * kT + threadIdx.x;
+        o4[2 * c] = make_uint4(st[w[0] & 0xFFFFu], st[w[0] >> 16], st[w[1] & 0xFFFFu], st[w[1] >> 16]);
+        o4[2 * c + 1] = make_uint4(st[w[2] & 0xFFFFu], st[w[2] >> 16], st[w[3] & 0xFFFFu], st[w[3] >> 16]);
+      }
+    } else {
 #pragma unroll
       for (int k = 0; k < VPT; k++) {
         const uint32_t i = k * kT + threadIdx.x;
-        if (i < m) out[t0 + i] = staged[pm[k]];
+        if (i < m) out[t0 + i] = st[pm[k]];
       }
     }
-    if (kLevel == 1 && threadIdx.x < nb) base[threadIdx.x] += toff[threadIdx.x + 1] - toff[threadIdx.x];
+    fence_proxy_async();  // generic reads of this buffer before the next bulk writes into it
+    __syncthreads();      // buffer cur free; tile it+1's expect_tx all posted
+    if (more && threadIdx.x == 0) mbar_arrive(bar + nxt);
   }
 }
 
@@ -1043,10 +1080,12 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
 }
 
 // Fine bins above the smem capacity (high-duplicate inputs): the bin's keys
-// stream from global memory twice while the 2^s counters stay in smem; lanes
-// of a warp that hit the same bucket (the common case here) share one atomic.
-// When `copy` is set the bin is first copied from `edges` into `src` (same
-// offsets) so placement can overwrite edges.
+// stream from global memory twice while the 2^s counters stay in smem.  Lanes
+// of a warp that hit the same bucket (the common case here: few distinct keys,
+// thousands of copies each) share one atomic (match_any), and the rank of each
+// lane inside its group comes from the group mask.  When `copy` is set the
+// count pass also copies the bin from `edges` into `src` (same offsets) so
+// placement can overwrite edges.
 template <typename H>
 __global__ void __launch_bounds__(1024)
 k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
@@ -1056,47 +1095,54 @@ k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_sta
   (void)scratch;
   extern __shared__ uint32_t cnt[];  // 2^s counters
   const uint32_t S = 1u << s;
-  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
   for (uint32_t k = blockIdx.x; k < *big_count; k += gridDim.x) {
     const uint32_t f = big_list[k];
     const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
     const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
-    if (copy)
-      for (uint32_t j = lo + threadIdx.x; j < hi; j += blockDim.x) src[j] = edges[j];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    const uint32_t rounds = (hi - lo + blockDim.x - 1) / blockDim.x;
-    for (uint32_t r = 0; r < rounds; r++) {
-      const uint32_t j = lo + r * blockDim.x + threadIdx.x;
-      const bool ok = j < hi;
-      const uint32_t l = ok ? H::bucket(src[j], hp) - (uint32_t)first : 0u;
-      const uint32_t act = __ballot_sync(0xffffffffu, ok);
-      const uint32_t l0 = __shfl_sync(0xffffffffu, l, act ? __ffs(act) - 1 : 0);
-      if (__all_sync(0xffffffffu, !ok || l == l0)) {
-        if (act && lane == __ffs(act) - 1) atomicAdd(cnt + l0, (uint32_t)__popc(act));
-      } else if (ok) {
-        atomicAdd(cnt + l, 1u);
+    // U keys per thread per round, loads first (the loop is latency-bound otherwise)
+    constexpr int U = 4;
+    const uint32_t step = U * blockDim.x;
+    for (uint32_t r0 = lo; r0 < hi; r0 += step) {
+      K kv[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
+        kv[u] = j < hi ? (copy ? edges[j] : src[j]) : K(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
+        const bool ok = j < hi;
+        if (ok && copy) src[j] = kv[u];
+        const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, l);
+        if (ok && (peers & lt) == 0) atomicAdd(cnt + l, (uint32_t)__popc(peers));
       }
     }
     __syncthreads();
     block_exscan_rows(cnt, nb, lo);
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = cnt[i];
     __syncthreads();
-    for (uint32_t r = 0; r < rounds; r++) {
-      const uint32_t j = lo + r * blockDim.x + threadIdx.x;
-      const bool ok = j < hi;
-      const K key = ok ? src[j] : K(0);
-      const uint32_t l = ok ? H::bucket(key, hp) - (uint32_t)first : 0u;
-      const uint32_t act = __ballot_sync(0xffffffffu, ok);
-      const uint32_t l0 = __shfl_sync(0xffffffffu, l, act ? __ffs(act) - 1 : 0);
-      if (__all_sync(0xffffffffu, !ok || l == l0)) {
+    for (uint32_t r0 = lo; r0 < hi; r0 += step) {
+      K kv[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
+        kv[u] = j < hi ? src[j] : K(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const bool ok = r0 + u * blockDim.x + threadIdx.x < hi;
+        const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, l);
         uint32_t b0 = 0;
-        if (act && lane == __ffs(act) - 1) b0 = atomicAdd(cnt + l0, (uint32_t)__popc(act));
-        b0 = __shfl_sync(0xffffffffu, b0, act ? __ffs(act) - 1 : 0);
-        if (ok) edges[b0 + __popc(act & lanemask_lt())] = key;
-      } else if (ok) {
-        edges[atomicAdd(cnt + l, 1u)] = key;
+        if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
+        b0 = __shfl_sync(0xffffffffu, b0, __ffs(peers) - 1);
+        if (ok) edges[b0 + __popc(peers & lt)] = kv[u];
       }
     }
     __syncthreads();
@@ -1156,24 +1202,10 @@ __device__ __forceinline__ uint32_t map_slot(K key) {
   return (uint32_t)(fmix64((uint64_t)key) & (kMapSlots - 1));
 }
 
-// Add one occurrence of `key` (lanes with ok == false only join the warp
-// aggregation); equal keys inside a warp are merged with one atomic.
+// Add `add` occurrences of `key` (per lane; a slot is claimed with CAS and
+// published once its key is written).
 template <typename K>
-__device__ __forceinline__ void map_add(BigMap<K>& m, K key, bool ok) {
-  const uint32_t act = __ballot_sync(0xffffffffu, ok);
-  if (!act) return;
-  const int first_lane = __ffs(act) - 1;
-  const K k0 = __shfl_sync(0xffffffffu, key, first_lane);
-  const bool same = __all_sync(0xffffffffu, !ok || key == k0);  // deep buckets: usually one key
-  if (!ok) return;
-  uint32_t peers;
-  if (same) {
-    peers = act;
-  } else {
-    peers = __match_any_sync(act, key);
-  }
-  if ((threadIdx.x & 31) != __ffs(peers) - 1) return;
-  const uint32_t add = __popc(peers);
+__device__ __forceinline__ void map_add_n(BigMap<K>& m, K key, uint32_t add) {
   uint32_t i = map_slot(key);
   for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
     uint32_t st = atomicCAS(&m.state[i], 0u, 1u);
@@ -1184,7 +1216,7 @@ __device__ __forceinline__ void map_add(BigMap<K>& m, K key, bool ok) {
       atomicAdd(&m.cnt[i], add);
       return;
     }
-    while (st == 1) st = atomicAdd(&m.state[i], 0u);  // another lane is publishing this slot
+    while (st == 1) st = atomicAdd(&m.state[i], 0u);  // another thread is publishing this slot
     if (*reinterpret_cast<volatile const K*>(&m.key[i]) == key) {
       atomicAdd(&m.cnt[i], add);
       return;
@@ -1391,34 +1423,33 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   // small smem map key -> occurrences, built once per bin, instead of an
   // O(degree) scan per query (the map was cleared before staging).
   if (s_deep) {
-    // each warp scans 32 consecutive buckets per round and feeds the deep
-    // ones (ballot) to the map cooperatively
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t l0 = (uint32_t)warp * 32; l0 < nb; l0 += blockDim.x) {
-      const uint32_t l = l0 + lane;
-      uint32_t a = 0, e = 0;
-      if (l < nb) {
-        if (in_smem) {
-          a = off16[l];
-          e = off16[l + 1];
-        } else {
-          a = t_off[first + l] - tlo;
-          e = t_off[first + l + 1] - tlo;
-        }
+    // All warps walk the slice's edges (warp w owns a contiguous range of
+    // 32-edge rows; lane j sees every 32nd edge of it).  Each lane counts runs
+    // of equal keys and adds a run to the map when its key changes, so a deep
+    // bucket holding one repeated key costs a few map updates spread over the
+    // whole CTA instead of one warp-serial update per 32 keys.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t rows = (tn + 31) / 32;
+    const uint32_t per = (rows + nw - 1) / nw;
+    const uint32_t r1 = min(rows, (uint32_t)(warp + 1) * per);
+    K cur = K(0);
+    uint32_t run = 0;
+    bool cur_deep = false;
+    for (uint32_t r = (uint32_t)warp * per; r < r1; r++) {
+      const uint32_t t = r * 32 + lane;
+      if (t >= tn) break;
+      const K key = in_smem ? te[t] : t_edges[tlo + t];
+      if (run == 0 || key != cur) {
+        if (run && cur_deep) map_add_n(map, cur, run);
+        cur = key;
+        run = 0;
+        const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
+        const uint32_t d = in_smem ? (uint32_t)off16[l + 1] - off16[l] : t_off[first + l + 1] - t_off[first + l];
+        cur_deep = d > kBigDeg;
       }
-      uint32_t deep = __ballot_sync(0xffffffffu, e - a > kBigDeg);
-      while (deep) {
-        const int src = __ffs(deep) - 1;
-        deep &= deep - 1;
-        const uint32_t ba = __shfl_sync(0xffffffffu, a, src), be = __shfl_sync(0xffffffffu, e, src);
-        for (uint32_t t0 = ba; t0 < be; t0 += 32) {
-          const uint32_t t = t0 + lane;
-          const bool ok = t < be;
-          const K key = ok ? (in_smem ? te[t] : t_edges[tlo + t]) : K(0);
-          map_add(map, key, ok);
-        }
-      }
+      run++;
     }
+    if (run && cur_deep) map_add_n(map, cur, run);
   }
   __syncthreads();
   const bool overflow = map.full != 0;
@@ -1441,7 +1472,7 @@ static size_t probe_smem(int s, int key_bits) {
          (key_bits == 32 ? (LocalShape<uint32_t>::kCap + 8) * 4 + sizeof(BigMap<uint32_t>)
                          : (LocalShape<uint64_t>::kCap + 8) * 8 + sizeof(BigMap<uint64_t>));
 }
-static size_t unpart_smem() { return (8192 + kPadMod * kMaxBins + 2 * kPadMod + 3 * kMaxBins + 4) * 4 + 16; }
+static size_t unpart_smem() { return (2 * kUnpStaged + 2 * (kMaxBins + 1) + 2 * kMaxBins + kMaxBins + 1) * 4 + 16; }
 
 size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query) {
   const size_t kb = key_bits / 8;

@@ -220,7 +220,8 @@ def test_all_identical_keys_large():
     assert res.multiplicities.tolist() == [n, 0, n]
 
 
-@pytest.mark.parametrize("n,values,lf", [(1 << 20, 1 << 8, 1.0), (1 << 22, 1 << 12, 1.0), ((1 << 20) + 5, 3, 2.0)])
+@pytest.mark.parametrize("n,values,lf", [(1 << 20, 1 << 8, 1.0), (1 << 22, 1 << 12, 1.0), ((1 << 20) + 5, 3, 2.0),
+                                         (1 << 22, 1 << 17, 1.0)])  # last: > 256 deep keys per bin (map overflow)
 def test_high_duplicate_build_and_query(n, values, lf):
     """C3-shaped inputs (many copies of few values): deep buckets go through the
     probe's per-bin map and oversized fine bins through the global build."""
