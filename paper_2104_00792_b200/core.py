@@ -8,14 +8,15 @@ access, so code written against the reference keeps working unchanged.
 
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _device as D
 from . import _lib
-from .errors import ConfigError
-from .hashing import HashFamily, family_code, hash_key, hash_range_for
+from .errors import ConfigError, SnapshotFormatError
+from .hashing import HashFamily, HashKind, family_code, hash_key, hash_range_for
 
 MASK32 = 0xFFFFFFFF
 
@@ -177,3 +178,65 @@ def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_p
     offsets, edges, positions = build_device(dk, v, family, key_bits, want_positions)
     table = HashGraph(offsets, edges, v, family, float(load_factor), key_bits, n)
     return table, BuildCounters(hashed=n, counted=n, placed=n), positions
+
+
+# ---------------------------------------------------------------- snapshots (core.py:27-28, 212-255)
+#
+# HGR1 is the reference's byte format: b"HGR1", header <QQBId (V, N, family
+# kind, seed, load factor), offsets as u64 LE [V+1], keys as u32 LE [N].  A
+# table over 64-bit keys is written as b"HGR8": the same header and offsets,
+# keys as u64 LE (the reference has no 64-bit tables).
+SNAPSHOT_MAGIC = {32: b"HGR1", 64: b"HGR8"}
+SNAPSHOT_HEADER = struct.Struct("<QQBId")
+
+
+def save_table(table, path) -> None:
+    """Write a table snapshot (core.py:212-225); the device CSR is widened on the GPU."""
+    t = as_device_table(table)
+    kind, seed = family_code(t.family)
+    with open(path, "wb") as f:
+        f.write(SNAPSHOT_MAGIC[t.key_bits])
+        f.write(SNAPSHOT_HEADER.pack(t.hash_range, t.num_keys, kind, seed, t.load_factor))
+        f.write(np.ascontiguousarray(t.offset, dtype="<u8").tobytes())
+        f.write(np.ascontiguousarray(t.keys, dtype="<u4" if t.key_bits == 32 else "<u8").tobytes())
+
+
+def read_snapshot(path):
+    """Parse and validate a snapshot on the host (core.py:228-255).
+
+    Returns (hash_range, family, load_factor, key_bits, offset int64[V+1], keys).
+    Raises SnapshotFormatError for a bad magic, a truncated header, an unknown
+    hash family, a body of the wrong length or a corrupt offset array."""
+    with open(path, "rb") as f:
+        blob = f.read()
+    bits = {m: b for b, m in SNAPSHOT_MAGIC.items()}.get(blob[:4])
+    if bits is None:
+        raise SnapshotFormatError(f"{path}: bad magic {blob[:4]!r}")
+    hdr = SNAPSHOT_HEADER.size
+    if len(blob) - 4 < hdr:
+        raise SnapshotFormatError(f"{path}: truncated header")
+    v, n, kind, seed, load_factor = SNAPSHOT_HEADER.unpack_from(blob, 4)
+    try:
+        family = HashFamily(HashKind(kind), seed)
+    except ValueError as e:
+        raise SnapshotFormatError(f"{path}: unknown hash family {kind}") from e
+    kb = bits // 8
+    if len(blob) - 4 != hdr + 8 * (v + 1) + kb * n:
+        raise SnapshotFormatError(f"{path}: body is {len(blob) - 4} bytes, expected "
+                                  f"{hdr + 8 * (v + 1) + kb * n} for V={v} N={n}")
+    offset = np.frombuffer(blob, dtype="<u8", count=v + 1, offset=4 + hdr).astype(np.int64)
+    keys = np.frombuffer(blob, dtype="<u4" if bits == 32 else "<u8", count=n, offset=4 + hdr + 8 * (v + 1))
+    keys = keys.astype(np.uint32 if bits == 32 else np.uint64)
+    if offset[0] != 0 or offset[-1] != n or (v > 0 and bool(np.any(offset[1:] < offset[:-1]))):
+        raise SnapshotFormatError(f"{path}: corrupt offset array")
+    return v, family, float(load_factor), bits, offset, keys
+
+
+def load_table(path) -> HashGraph:
+    """Read a snapshot into a device table (core.py:228-255)."""
+    v, family, load_factor, bits, offset, keys = read_snapshot(path)
+    D.require_cuda()
+    if len(keys) >= 1 << 32:
+        raise ConfigError("device tables hold fewer than 2^32 keys")
+    off_dev = D.torch().from_numpy(offset.astype(np.uint32).view(np.int32)).to(D.device())
+    return HashGraph(off_dev, D.to_device_keys(keys, bits), v, family, load_factor, bits)
