@@ -15,7 +15,7 @@ from collections import defaultdict
 rnd, launch_csv, rep = sys.argv[1], sys.argv[2], sys.argv[3]
 LABEL = {  # kernel function -> launch label used by the library / bench
     "k_hist": "hg_hist", "k_colscan": "hg_colscan", "k_starts": "hg_starts", "k_local_build_big": "hg_local_build_big",
-    "k_local_build": "hg_local_build", "k_local_probe": "hg_local_probe", "k_unpart<2>": "hg_unpart2",
+    "k_local_build": "hg_local_build", "k_local_build_p": "hg_local_build", "k_local_probe": "hg_local_probe", "k_unpart<2>": "hg_unpart2",
     "k_unpart<1>": "hg_unpart1", "k_count": "hg_count", "k_scan": "hg_scan", "k_place": "hg_place",
     "k_intersect": "hg_intersect", "k_generate32": "hg_generate",
 }
