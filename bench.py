@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--dist", action="store_true", help="use the partitioned (torch.distributed) path even at N=1")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="partitioned path's key exchange: fused peer-memory scatter (p2p) or NCCL alltoallv")
     return ap.parse_args()
 
 
@@ -268,7 +270,7 @@ def main():
     if use_dist:
         from paper_2104_00792_b200 import distributed as hd
 
-        cfg = hd.DistConfig(load_factor=args.load_factor, key_bits=kb)
+        cfg = hd.DistConfig(load_factor=args.load_factor, key_bits=kb, transport=args.transport)
 
         def step():
             table = hd.build_distributed(keys, cfg)
@@ -407,7 +409,7 @@ def main():
                                 + f", C={args.load_factor}"),
                    "keys_per_gpu": n, "queries_per_gpu": q, "hash_range_per_gpu": v,
                    "l2": "inputs (1 GiB per array) larger than the 126 MB L2",
-                   "parallelism": "single-shard" if not use_dist else f"partitioned over {world} GPU(s) (NCCL)",
+                   "parallelism": "single-shard" if not use_dist else f"partitioned over {world} GPU(s) ({'fused peer-memory exchange' if args.transport == 'p2p' else 'NCCL alltoallv'})",
                    "launch": "cuda_graph (one step captured, replayed per step)" if use_graph else "eager"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         "kernels": kernels,

@@ -117,6 +117,41 @@ HG_API int hg_reorganize(const void* keys, uint64_t n, int key_bits, int kind, u
                   uint64_t* row_offsets, void* grouped, uint32_t* order, uint64_t* search_steps,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Phase 2 + Phase 3 fused over peer memory (one process per GPU; the receive
+ * buffers are symmetric allocations mapped into every rank over NVLink /
+ * NVSwitch) -- replaces reorganize + exchange (multishard.py:294-333).
+ * hg_reorganize_count: count pass + scan, row_offsets uint64[shards+1] (device;
+ *   row sizes = send counts); per-tile bases stay in `workspace`.
+ * hg_reorganize_place_peers: same keys/splits/workspace; key i of row d is
+ *   stored at ((K*)dest_ptrs[d])[dest_base[d] + its stable rank in row d];
+ *   dest_ptrs / dest_base: uint64[shards] device arrays; order (nullable) as in
+ *   hg_reorganize (local grouped positions).
+ * hg_return_peers: reverse direction for uint32 answers: vals[i], i in sender
+ *   s's segment [recv_bounds[s], recv_bounds[s+1]) of this rank's receive
+ *   order, goes to ((uint32_t*)back_ptrs[s])[back_base[s] + i - recv_bounds[s]]. */
+HG_API int hg_reorganize_count(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
+                        uint64_t hash_range, uint64_t bin_size, const int64_t* splits, uint32_t shards,
+                        uint64_t* row_offsets, uint64_t* search_steps, void* workspace,
+                        size_t workspace_bytes, void* stream);
+HG_API int hg_reorganize_place_peers(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
+                              uint64_t hash_range, uint64_t bin_size, const int64_t* splits,
+                              uint32_t shards, const uint64_t* row_offsets, const uint64_t* dest_ptrs,
+                              const uint64_t* dest_base, uint32_t* order, void* workspace,
+                              size_t workspace_bytes, void* stream);
+/* Routing in one pass, for the distributed build and query when the
+ * per-destination counts are already known (segment sums of the Phase-1 bin
+ * histogram): per tile one claim per destination on cursors[d] (uint64[P]
+ * device scratch, zeroed by the call); key -> ((K*)dest_ptrs[d])[dest_base[d]
+ * + claim] when dest_ptrs is given (peer memory), else grouped[row_offsets[d]
+ * + claim]; order (nullable) [row_offsets[d] + claim] = input index.  Rows are
+ * complete but not in input order (see hg_reorganize for the stable form). */
+HG_API int hg_route(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,
+             uint64_t bin_size, const int64_t* splits, uint32_t shards, const uint64_t* row_offsets,
+             const uint64_t* dest_ptrs, const uint64_t* dest_base, void* grouped, uint32_t* order,
+             uint64_t* cursors, void* stream);
+HG_API int hg_return_peers(const uint32_t* vals, uint64_t n, const uint64_t* recv_bounds,
+                    const uint64_t* back_ptrs, const uint64_t* back_base, uint32_t shards, void* stream);
+
 /* Positional merge of per-shard multiplicities -- replaces
  * `multiplicities[order[off_d:off_d+1]] = res.multiplicities`
  * (multishard.py:523): out[order[i]] = src[i]. */

@@ -23,21 +23,45 @@ static inline int grid_cap(uint64_t n, int per_sm) {
 // flushed once per CTA with 64-bit atomics.  Falls back to global atomics for
 // very large bin counts (smem_bins == 0).
 template <typename K>
-__global__ void k_bin_hist(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin,
-                           uint32_t bins_g, int use_smem, unsigned long long* __restrict__ out) {
+__device__ __forceinline__ void bin_hist_add(K key, const HashParams& hp, const DivParams& bin, int use_smem,
+                                             uint32_t* s_hist, unsigned long long* out) {
+  const uint32_t b = (uint32_t)div_by(hash_mod(key, hp), bin);
+  if (use_smem) atomicAdd(s_hist + b, 1u);
+  else atomicAdd(out + b, 1ull);
+}
+
+// 16-byte loads, four in flight per thread (the loop is latency-bound with
+// one scalar load per iteration).
+template <typename K>
+__global__ void __launch_bounds__(1024) k_bin_hist(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin,
+                                                   uint32_t bins_g, int use_smem, unsigned long long* __restrict__ out) {
+  constexpr int VPL = 16 / sizeof(K);
   extern __shared__ uint32_t s_hist[];
   if (use_smem) {
     for (uint32_t i = threadIdx.x; i < bins_g; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
   }
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t b = (uint32_t)div_by(hash_mod(keys[i], hp), bin);
-    if (use_smem)
-      atomicAdd(s_hist + b, 1u);
-    else
-      atomicAdd(out + b, 1ull);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+    const uint4* p = reinterpret_cast<const uint4*>(keys);
+    const uint64_t nv = n / VPL;
+    for (uint64_t v = tid; v < nv; v += 4 * stride) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) q[u] = v + u * stride < nv ? __ldcs(p + v + u * stride) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        if (v + u * stride >= nv) break;
+        const K* qk = reinterpret_cast<const K*>(&q[u]);
+#pragma unroll
+        for (int j = 0; j < VPL; j++) bin_hist_add(qk[j], hp, bin, use_smem, s_hist, out);
+      }
+    }
+    done = nv * VPL;
   }
+  for (uint64_t i = done + tid; i < n; i += stride) bin_hist_add(keys[i], hp, bin, use_smem, s_hist, out);
   if (use_smem) {
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < bins_g; i += blockDim.x)
@@ -92,8 +116,8 @@ __global__ void k_split_plan(const unsigned long long* __restrict__ counts, uint
 // --------------------------------------------------------------------------- Phase 2
 
 constexpr int kReorgWarps = 8;
-constexpr int kReorgPerLane = 8;
-constexpr int kReorgTile = kReorgWarps * 32 * kReorgPerLane;  // 2048 keys per tile
+constexpr int kReorgPerLane = 16;
+constexpr int kReorgTile = kReorgWarps * 32 * kReorgPerLane;  // 4096 keys per tile
 
 // destination shard of a bin: #{d in 1..P-1 : splits[d] <= bin}, i.e.
 // searchsorted(boundaries, h, 'right') - 1 with boundaries = splits * bin_size
@@ -122,13 +146,20 @@ k_reorg_count(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * kReorgTile;
   unsigned long long st = 0;
-  for (int j = threadIdx.x; j < kReorgTile; j += blockDim.x) {
-    uint64_t i = base + j;
-    if (i < n) {
-      uint32_t d = dest_of_bin(div_by(hash_mod(keys[i], hp), bin), s_splits, shards);
-      atomicAdd(s_cnt + d, 1u);
-      st += d + 1;
-    }
+  K kv[kReorgPerLane];  // all loads in flight before any hashing
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    const uint64_t i = base + r * blockDim.x + threadIdx.x;
+    kv[r] = i < n ? keys[i] : K(0);
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    const bool ok = base + r * blockDim.x + threadIdx.x < n;
+    const uint32_t d = ok ? dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);  // one atomic per destination per round
+    if (ok && (peers & lt) == 0) atomicAdd(s_cnt + d, (uint32_t)__popc(peers));
+    st += ok ? d + 1 : 0u;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) st += __shfl_xor_sync(0xffffffffu, st, o);
@@ -191,35 +222,53 @@ __global__ void k_reorg_rows(const unsigned long long* __restrict__ totals, uint
 // Place pass: stable within a tile (warp w owns keys [w*256, (w+1)*256) of
 // the tile, processed in 32-key rounds in index order; ranks inside a round
 // come from ballots per distinct destination).
-template <typename K>
+//
+// kPeer: Phase 2 and Phase 3 fused -- each key is stored straight into its
+// destination rank's receive buffer (dest_ptrs[d], peer memory mapped over
+// NVLink / NVSwitch) at dest_base[d] + (its stable rank in row d); `order`
+// still records the input index at the local grouped position.
+template <typename K, bool kPeer>
 __global__ void __launch_bounds__(kReorgWarps * 32)
 k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin,
               const long long* __restrict__ splits, uint32_t shards,
               const uint32_t* __restrict__ tile_base, const unsigned long long* __restrict__ row_offsets,
-              K* __restrict__ grouped, uint32_t* __restrict__ order) {
+              K* __restrict__ grouped, uint32_t* __restrict__ order,
+              const unsigned long long* __restrict__ dest_ptrs, const unsigned long long* __restrict__ dest_base) {
   extern __shared__ unsigned char s_raw[];
   long long* s_splits = reinterpret_cast<long long*>(s_raw);
   unsigned long long* s_base = reinterpret_cast<unsigned long long*>(s_splits + shards + 1);
-  uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(s_base + shards);  // [warps][shards]
+  unsigned long long* s_rbase = s_base + shards;                      // kPeer: remote slot base per row
+  uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(s_rbase + (kPeer ? shards : 0));  // [warps][shards]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i <= shards; i += blockDim.x) s_splits[i] = splits[i];
-  for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x)
-    s_base[i] = row_offsets[i] + tile_base[(uint64_t)blockIdx.x * shards + i];
+  for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x) {
+    const uint32_t tb = tile_base[(uint64_t)blockIdx.x * shards + i];
+    s_base[i] = row_offsets[i] + tb;
+    if (kPeer) s_rbase[i] = dest_base[i] + tb;
+  }
   for (uint32_t i = threadIdx.x; i < kReorgWarps * shards; i += blockDim.x) s_wcnt[i] = 0;
   __syncthreads();
 
   const uint64_t wbase = (uint64_t)blockIdx.x * kReorgTile + (uint64_t)warp * 32 * kReorgPerLane;
+  const uint32_t lt = lanemask_lt();
+  uint32_t* my = s_wcnt + warp * shards;  // this warp's per-destination counts, then cursors
   K kv[kReorgPerLane];
   uint32_t dv[kReorgPerLane];
 #pragma unroll
   for (int r = 0; r < kReorgPerLane; r++) {
-    uint64_t i = wbase + r * 32 + lane;
-    dv[r] = 0xffffffffu;
-    if (i < n) {
-      kv[r] = keys[i];
-      dv[r] = dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards);
-      atomicAdd(s_wcnt + warp * shards + dv[r], 1u);
-    }
+    const uint64_t i = wbase + r * 32 + lane;
+    kv[r] = i < n ? keys[i] : K(0);
+  }
+  // count: lanes of a round with the same destination (match_any) are
+  // counted once by their lowest lane; the warp owns its row, so the
+  // increments need no atomics
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    const bool ok = wbase + r * 32 + lane < n;
+    dv[r] = ok ? dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dv[r]);
+    if (ok && (peers & lt) == 0) my[dv[r]] += __popc(peers);
+    __syncwarp();
   }
   __syncthreads();
   // exclusive prefix over warps, per destination
@@ -232,28 +281,120 @@ k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
     }
   }
   __syncthreads();
-  uint32_t* my = s_wcnt + warp * shards;  // running per-destination cursor of this warp
+  // place: a round's lanes with the same destination take consecutive slots
+  // in lane order after the warp's cursor (stable: rounds, then lanes, in
+  // input order)
 #pragma unroll
   for (int r = 0; r < kReorgPerLane; r++) {
     const uint32_t d = dv[r];
-    uint32_t active = __ballot_sync(0xffffffffu, d != 0xffffffffu);
-    uint32_t slot_rank = 0, slot_d = d;
-    while (active) {
-      const int leader = __ffs(active) - 1;
-      const uint32_t d0 = __shfl_sync(0xffffffffu, d, leader);
-      const uint32_t m = __ballot_sync(0xffffffffu, d == d0) & active;
-      uint32_t cur = my[d0];
-      if (d == d0) slot_rank = cur + __popc(m & lanemask_lt());
-      __syncwarp();
-      if (lane == leader) my[d0] = cur + __popc(m);
-      __syncwarp();
-      active &= ~m;
-    }
-    if (d != 0xffffffffu) {
-      unsigned long long slot = s_base[slot_d] + slot_rank;
-      grouped[slot] = kv[r];
+    const bool ok = d != 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t cur = ok ? my[d] : 0u;
+    __syncwarp();
+    if (ok && (peers & lt) == 0) my[d] = cur + __popc(peers);
+    __syncwarp();
+    if (ok) {
+      const uint32_t rank = cur + __popc(peers & lt);
+      const unsigned long long slot = s_base[d] + rank;
+      if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[s_rbase[d] + rank] = kv[r];
+      else grouped[slot] = kv[r];
       if (order) order[slot] = (uint32_t)(wbase + r * 32 + lane);
     }
+  }
+  if (kPeer) __threadfence_system();  // peer stores ordered before the barrier that publishes them
+}
+
+// Routing without a count pass (the distributed build and query): per tile,
+// each key's destination and its rank among the warp's keys for that
+// destination (match_any), per-warp prefix, then ONE global claim per
+// (tile, destination) on cursors[d]; the key goes to slot dest_base[d] +
+// claim (peer memory, kPeer) or row_offsets[d] + claim (local grouped
+// buffer), and order[row_offsets[d] + claim] = its input index.  Each warp
+// round writes a contiguous run per destination.  Rows hold the right keys
+// but not in input order (claims race), which the local build and the
+// positional query merge do not need; the reference-order API
+// (hg_reorganize) keeps the stable two-pass kernels.  (Staging the tile in
+// smem to write one run per destination measured slower.)
+template <typename K, bool kPeer>
+__global__ void __launch_bounds__(kReorgWarps * 32)
+k_route_claim(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin, const long long* __restrict__ splits,
+              uint32_t shards, const unsigned long long* __restrict__ row_offsets,
+              const unsigned long long* __restrict__ dest_ptrs, const unsigned long long* __restrict__ dest_base,
+              K* __restrict__ grouped, uint32_t* __restrict__ order, unsigned long long* __restrict__ cursors) {
+  extern __shared__ unsigned char s_raw[];
+  long long* s_splits = reinterpret_cast<long long*>(s_raw);
+  unsigned long long* s_tb = reinterpret_cast<unsigned long long*>(s_splits + shards + 1);  // claim base per d
+  uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(s_tb + shards);                              // [warps][shards]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t i = threadIdx.x; i <= shards; i += blockDim.x) s_splits[i] = splits[i];
+  for (uint32_t i = threadIdx.x; i < kReorgWarps * shards; i += blockDim.x) s_wcnt[i] = 0;
+  const uint64_t wbase = (uint64_t)blockIdx.x * kReorgTile + (uint64_t)warp * 32 * kReorgPerLane;
+  K kv[kReorgPerLane];
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    const uint64_t i = wbase + r * 32 + lane;
+    kv[r] = i < n ? keys[i] : K(0);
+  }
+  __syncthreads();
+  uint32_t* my = s_wcnt + warp * shards;
+  uint32_t dr[kReorgPerLane];  // destination << 16 | rank inside the warp's keys for it (or ~0)
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    const bool ok = wbase + r * 32 + lane < n;
+    const uint32_t d = ok ? dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t cur = ok ? my[d] : 0u;
+    __syncwarp();
+    if (ok && (peers & lt) == 0) my[d] = cur + __popc(peers);
+    __syncwarp();
+    dr[r] = ok ? (d << 16) | (cur + __popc(peers & lt)) : 0xffffffffu;
+  }
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < shards; d += blockDim.x) {
+    uint32_t run = 0;
+    for (int w = 0; w < kReorgWarps; w++) {
+      const uint32_t c = s_wcnt[w * shards + d];
+      s_wcnt[w * shards + d] = run;
+      run += c;
+    }
+    s_tb[d] = run ? atomicAdd(cursors + d, (unsigned long long)run) : 0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kReorgPerLane; r++) {
+    if (dr[r] == 0xffffffffu) continue;
+    const uint32_t d = dr[r] >> 16;
+    const unsigned long long c = s_tb[d] + my[d] + (dr[r] & 0xFFFFu);
+    if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[dest_base[d] + c] = kv[r];
+    else grouped[row_offsets[d] + c] = kv[r];
+    if (order) order[row_offsets[d] + c] = (uint32_t)(wbase + r * 32 + lane);
+  }
+  if (kPeer) __threadfence_system();
+}
+
+// Reverse exchange over peer memory: element i of this rank's receive order
+// belongs to sender s with recv_bounds[s] <= i < recv_bounds[s+1]; its value
+// goes to sender s's buffer back_ptrs[s] at back_base[s] + (i - recv_bounds[s])
+// (the sender's grouped position of that key).  Contiguous per sender, so the
+// peer stores coalesce.
+__global__ void k_return_peers(const uint32_t* __restrict__ vals, uint64_t n, const unsigned long long* __restrict__ recv_bounds,
+                               const unsigned long long* __restrict__ back_ptrs,
+                               const unsigned long long* __restrict__ back_base, uint32_t shards) {
+  extern __shared__ unsigned long long s_rb[];  // recv_bounds (P+1), back_base (P), back_ptrs (P)
+  for (uint32_t i = threadIdx.x; i <= shards; i += blockDim.x) s_rb[i] = recv_bounds[i];
+  for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x) {
+    s_rb[shards + 1 + i] = back_base[i];
+    s_rb[2 * shards + 1 + i] = back_ptrs[i];
+  }
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = shards;  // last s with recv_bounds[s] <= i
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_rb[mid] <= i) lo = mid; else hi = mid;
+    }
+    reinterpret_cast<uint32_t*>(s_rb[2 * shards + 1 + lo])[s_rb[shards + 1 + lo] + (i - s_rb[lo])] = vals[i];
   }
 }
 
@@ -261,8 +402,19 @@ k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
 
 __global__ void k_scatter_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ order, uint64_t n,
                               uint32_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[order[i]] = src[i];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    uint32_t o[4], v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint64_t j = i + u * stride;
+      o[u] = j < n ? __ldcs(order + j) : 0u;
+      v[u] = j < n ? __ldcs(src + j) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (i + u * stride < n) out[o[u]] = v[u];
+  }
 }
 
 __global__ void k_widen_u32(const uint32_t* __restrict__ src, uint64_t n, long long* __restrict__ out) {
@@ -291,6 +443,58 @@ static int check_hash(int key_bits, int kind, uint64_t v) {
   if (key_bits != 32 && key_bits != 64) return set_error(HG_ERR_CONFIG, "key_bits must be 32 or 64, got %d", key_bits);
   if (kind != HG_KIND_MURMUR32 && kind != HG_KIND_IDENTITY) return set_error(HG_ERR_CONFIG, "unknown hash kind %d", kind);
   if (v < 1) return set_error(HG_ERR_CONFIG, "hash range must be >= 1");
+  return HG_OK;
+}
+
+// Count pass + column scan + row offsets; tile bases stay in the workspace for
+// the place pass (hg_reorganize or hg_reorganize_place_peers).
+static int reorg_count(const void* keys, uint64_t n, int key_bits, const HashParams& hp, const DivParams& dp,
+                       const int64_t* splits, uint32_t shards, uint64_t* row_offsets, uint64_t* search_steps,
+                       uint32_t* tile_counts, unsigned long long* totals, cudaStream_t s) {
+  const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  const size_t smem_c = 8 * (shards + 1) + 4 * shards;
+  if (key_bits == 32) {
+    HG_LAUNCH("hg_reorg_count", k_reorg_count<uint32_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
+              (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
+              (unsigned long long*)search_steps);
+  } else {
+    HG_LAUNCH("hg_reorg_count", k_reorg_count<uint64_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
+              (const uint64_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
+              (unsigned long long*)search_steps);
+  }
+  HG_LAUNCH("hg_reorg_scan", k_reorg_scan, shards, 1024, 0, s, tile_counts, tiles, shards, totals);
+  HG_LAUNCH("hg_reorg_rows", k_reorg_rows, 1, 32, 0, s, totals, shards, (unsigned long long*)row_offsets);
+  return HG_OK;
+}
+
+template <bool kPeer>
+static int reorg_place(const void* keys, uint64_t n, int key_bits, const HashParams& hp, const DivParams& dp,
+                       const int64_t* splits, uint32_t shards, const uint32_t* tile_counts, const uint64_t* row_offsets,
+                       void* grouped, uint32_t* order, const uint64_t* dest_ptrs, const uint64_t* dest_base,
+                       cudaStream_t s) {
+  const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  const size_t smem_p = 8 * (shards + 1) + 8 * shards * (kPeer ? 2 : 1) + 4 * kReorgWarps * shards;
+  const auto* ro = (const unsigned long long*)row_offsets;
+  const auto* dp_ = (const unsigned long long*)dest_ptrs;
+  const auto* db = (const unsigned long long*)dest_base;
+  if (key_bits == 32) {
+    HG_LAUNCH("hg_reorg_place", (k_reorg_place<uint32_t, kPeer>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
+              (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, (uint32_t*)grouped,
+              order, dp_, db);
+  } else {
+    HG_LAUNCH("hg_reorg_place", (k_reorg_place<uint64_t, kPeer>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
+              (const uint64_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, (uint64_t*)grouped,
+              order, dp_, db);
+  }
+  return HG_OK;
+}
+
+static int reorg_check(int key_bits, int kind, uint64_t hash_range, uint32_t shards, uint64_t bin_size, uint64_t n) {
+  int rc = check_hash(key_bits, kind, hash_range);
+  if (rc) return rc;
+  if (shards < 1 || shards > 4096) return set_error(HG_ERR_CONFIG, "shard count must be in [1, 4096], got %u", shards);
+  if (bin_size < 1) return set_error(HG_ERR_CONFIG, "bin_size must be >= 1");
+  if (n >= (1ull << 32)) return set_error(HG_ERR_CONFIG, "a shard holds fewer than 2^32 keys");
   return HG_OK;
 }
 
@@ -347,11 +551,8 @@ size_t hg_reorganize_workspace_size(uint64_t n, uint32_t shards) {
 int hg_reorganize(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,
                   uint64_t bin_size, const int64_t* splits, uint32_t shards, uint64_t* row_offsets, void* grouped,
                   uint32_t* order, uint64_t* search_steps, void* workspace, size_t workspace_bytes, void* stream) {
-  int rc = check_hash(key_bits, kind, hash_range);
+  int rc = reorg_check(key_bits, kind, hash_range, shards, bin_size, n);
   if (rc) return rc;
-  if (shards < 1 || shards > 4096) return set_error(HG_ERR_CONFIG, "shard count must be in [1, 4096], got %u", shards);
-  if (bin_size < 1) return set_error(HG_ERR_CONFIG, "bin_size must be >= 1");
-  if (n >= (1ull << 32)) return set_error(HG_ERR_CONFIG, "a shard holds fewer than 2^32 keys");
   cudaStream_t s = (cudaStream_t)stream;
   uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
   Workspace ws{(char*)workspace, workspace_bytes, 0};
@@ -364,28 +565,104 @@ int hg_reorganize(const void* keys, uint64_t n, int key_bits, int kind, uint32_t
   }
   HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
   DivParams dp = make_div_params(bin_size);
-  size_t smem_c = 8 * (shards + 1) + 4 * shards;
-  size_t smem_p = 8 * (shards + 1) + 8 * shards + 4 * kReorgWarps * shards;
-  if (key_bits == 32) {
-    HG_LAUNCH("hg_reorg_count", k_reorg_count<uint32_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
-              (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
-              (unsigned long long*)search_steps);
-  } else {
-    HG_LAUNCH("hg_reorg_count", k_reorg_count<uint64_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
-              (const uint64_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
-              (unsigned long long*)search_steps);
+  rc = reorg_count(keys, n, key_bits, hp, dp, splits, shards, row_offsets, search_steps, tile_counts, totals, s);
+  if (rc) return rc;
+  return reorg_place<false>(keys, n, key_bits, hp, dp, splits, shards, tile_counts, row_offsets, grouped, order,
+                            nullptr, nullptr, s);
+}
+
+int hg_reorganize_count(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,
+                        uint64_t bin_size, const int64_t* splits, uint32_t shards, uint64_t* row_offsets,
+                        uint64_t* search_steps, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = reorg_check(key_bits, kind, hash_range, shards, bin_size, n);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  Workspace ws{(char*)workspace, workspace_bytes, 0};
+  uint32_t* tile_counts = ws.take<uint32_t>(tiles * shards);
+  unsigned long long* totals = ws.take<unsigned long long>(shards);
+  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "reorganize workspace too small");
+  if (!n) {
+    HG_CHECK_CUDA(cudaMemsetAsync(row_offsets, 0, 8 * ((uint64_t)shards + 1), s));
+    return HG_OK;
   }
-  HG_LAUNCH("hg_reorg_scan", k_reorg_scan, shards, 1024, 0, s, tile_counts, tiles, shards, totals);
-  HG_LAUNCH("hg_reorg_rows", k_reorg_rows, 1, 32, 0, s, totals, shards, (unsigned long long*)row_offsets);
+  HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
+  DivParams dp = make_div_params(bin_size);
+  return reorg_count(keys, n, key_bits, hp, dp, splits, shards, row_offsets, search_steps, tile_counts, totals, s);
+}
+
+int hg_reorganize_place_peers(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
+                              uint64_t hash_range, uint64_t bin_size, const int64_t* splits, uint32_t shards,
+                              const uint64_t* row_offsets, const uint64_t* dest_ptrs, const uint64_t* dest_base,
+                              uint32_t* order, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = reorg_check(key_bits, kind, hash_range, shards, bin_size, n);
+  if (rc) return rc;
+  if (!n) return HG_OK;
+  if (!dest_ptrs || !dest_base) return set_error(HG_ERR_CONFIG, "dest_ptrs and dest_base are required");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  Workspace ws{(char*)workspace, workspace_bytes, 0};
+  uint32_t* tile_counts = ws.take<uint32_t>(tiles * shards);
+  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "reorganize workspace too small");
+  HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
+  DivParams dp = make_div_params(bin_size);
+  return reorg_place<true>(keys, n, key_bits, hp, dp, splits, shards, tile_counts, row_offsets, nullptr, order,
+                           dest_ptrs, dest_base, s);
+}
+
+int hg_route(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,
+             uint64_t bin_size, const int64_t* splits, uint32_t shards, const uint64_t* row_offsets,
+             const uint64_t* dest_ptrs, const uint64_t* dest_base, void* grouped, uint32_t* order, uint64_t* cursors,
+             void* stream) {
+  int rc = reorg_check(key_bits, kind, hash_range, shards, bin_size, n);
+  if (rc) return rc;
+  if (shards > 65535) return set_error(HG_ERR_CONFIG, "hg_route supports at most 65535 shards");
+  cudaStream_t s = (cudaStream_t)stream;
+  HG_CHECK_CUDA(cudaMemsetAsync(cursors, 0, 8 * (size_t)shards, s));
+  if (!n) return HG_OK;
+  const bool peer = dest_ptrs != nullptr;
+  if (peer && !dest_base) return set_error(HG_ERR_CONFIG, "dest_base is required with dest_ptrs");
+  if (!peer && !grouped) return set_error(HG_ERR_CONFIG, "grouped is required without dest_ptrs");
+  HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
+  DivParams dp = make_div_params(bin_size);
+  const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  const size_t smem = 8 * (shards + 1) + 8 * (size_t)shards + 4 * (size_t)kReorgWarps * shards;
+  if (smem > 200 * 1024) return set_error(HG_ERR_CONFIG, "too many shards for hg_route (%u)", shards);
+  const auto* ro = (const unsigned long long*)row_offsets;
+  const auto* dpt = (const unsigned long long*)dest_ptrs;
+  const auto* db = (const unsigned long long*)dest_base;
+  auto* cur = (unsigned long long*)cursors;
+  const auto* sp = (const long long*)splits;
   if (key_bits == 32) {
-    HG_LAUNCH("hg_reorg_place", k_reorg_place<uint32_t>, (unsigned)tiles, kReorgWarps * 32, smem_p, s,
-              (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
-              (const unsigned long long*)row_offsets, (uint32_t*)grouped, order);
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (peer)
+      HG_LAUNCH("hg_route", (k_route_claim<uint32_t, true>), (unsigned)tiles, kReorgWarps * 32, smem, s,
+                (const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur);
+    else
+      HG_LAUNCH("hg_route", (k_route_claim<uint32_t, false>), (unsigned)tiles, kReorgWarps * 32, smem, s,
+                (const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur);
   } else {
-    HG_LAUNCH("hg_reorg_place", k_reorg_place<uint64_t>, (unsigned)tiles, kReorgWarps * 32, smem_p, s,
-              (const uint64_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
-              (const unsigned long long*)row_offsets, (uint64_t*)grouped, order);
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (peer)
+      HG_LAUNCH("hg_route", (k_route_claim<uint64_t, true>), (unsigned)tiles, kReorgWarps * 32, smem, s,
+                (const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur);
+    else
+      HG_LAUNCH("hg_route", (k_route_claim<uint64_t, false>), (unsigned)tiles, kReorgWarps * 32, smem, s,
+                (const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur);
   }
+  return HG_OK;
+}
+
+int hg_return_peers(const uint32_t* vals, uint64_t n, const uint64_t* recv_bounds, const uint64_t* back_ptrs,
+                    const uint64_t* back_base, uint32_t shards, void* stream) {
+  if (shards < 1 || shards > 4096) return set_error(HG_ERR_CONFIG, "shard count must be in [1, 4096], got %u", shards);
+  if (!n) return HG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  HG_LAUNCH("hg_return_peers", k_return_peers, grid_cap(n, 8), kT, 8 * (3 * (size_t)shards + 1), s, vals, n,
+            (const unsigned long long*)recv_bounds, (const unsigned long long*)back_ptrs,
+            (const unsigned long long*)back_base, shards);
   return HG_OK;
 }
 

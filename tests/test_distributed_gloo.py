@@ -60,6 +60,22 @@ class OracleOps:
         grouped = torch.from_numpy(k[order].view(np.int32).copy())
         return torch.from_numpy(offs), grouped, torch.from_numpy(order.astype(np.int32))
 
+    def segment_sums(self, local_counts, splits):
+        cs = np.concatenate([[0], np.cumsum(local_counts.numpy())])
+        sp = splits.numpy()
+        return torch.from_numpy((cs[sp[1:]] - cs[sp[:-1]]).astype(np.int64))
+
+    def route(self, keys, hr, bin_size, splits, shards, family, row_offsets, dest_ptrs=None, dest_base=None,
+              want_order=False):
+        offs, grouped, order = self.reorganize(keys, hr, bin_size, splits, shards, family, want_order=True)
+        offs = offs.numpy()
+        assert np.array_equal(offs[:-1], np.asarray(row_offsets))  # counts from the histogram == real row sizes
+        # hg_route's claims race: any order inside a row is valid -- shuffle rows to prove nothing depends on it
+        rng = np.random.default_rng(len(grouped))
+        perm = np.concatenate([offs[d] + rng.permutation(offs[d + 1] - offs[d]) for d in range(shards)]).astype(np.int64)
+        perm = torch.from_numpy(perm)
+        return grouped[perm], (order[perm] if want_order else None)
+
     def build(self, keys, v, family, load_factor):
         off, placed, _ = O.build_csr(self._np(keys), v, self.kind, self.seed)
         return OracleTable(off, placed, v)
@@ -133,3 +149,49 @@ def test_build_and_query_distributed_match_reference(world, n, dom, kind, seed, 
     agg = outs[0]["agg"]
     assert (int(agg[0]), int(agg[1]), int(agg[2])) == (matched, total, comp)
     assert outs[0]["hv"] == hv
+
+
+# ---- fused peer-memory exchange: slot arithmetic (no GPU, no process group)
+
+def _emulate_p2p(rows_per_sender, rank_of_dest_layouts):
+    """Place every sender's row d at dest_base into receiver d's buffer, as
+    hg_reorganize_place_peers does, and return the receive buffers."""
+    P = len(rows_per_sender)
+    mat = np.array([[len(rows_per_sender[s][d]) for d in range(P)] for s in range(P)])
+    from paper_2104_00792_b200.distributed import peer_layout
+
+    lays = [peer_layout(mat, r) for r in range(P)]
+    recv = [np.full(lays[d]["n_recv"], -1, dtype=np.int64) for d in range(P)]
+    for s in range(P):
+        for d in range(P):
+            row = rows_per_sender[s][d]
+            b = lays[s]["dest_base"][d]
+            assert np.all(recv[d][b:b + len(row)] == -1), "overlapping peer writes"
+            recv[d][b:b + len(row)] = row
+    return mat, lays, recv
+
+
+@pytest.mark.parametrize("P,seed", [(1, 0), (2, 1), (3, 2), (8, 3), (8, 4)])
+def test_peer_layout_equals_alltoallv(P, seed):
+    rng = np.random.default_rng(seed)
+    rows = [[rng.integers(0, 1 << 30, size=int(rng.integers(0, 50) if rng.random() > 0.2 else 0)) for _ in range(P)]
+            for _ in range(P)]
+    mat, lays, recv = _emulate_p2p(rows, None)
+    for d in range(P):
+        # ExchangeFabric.gather(d): senders' rows in rank order (multishard.py:137-166)
+        expect = np.concatenate([rows[s][d] for s in range(P)]) if P else np.zeros(0)
+        assert np.array_equal(recv[d], expect)
+        assert lays[d]["n_recv"] == mat[:, d].sum()
+        assert lays[d]["capacity"] == mat.sum(axis=0).max()
+    # reverse direction: receiver d's element i of sender s's segment goes back
+    # to s's grouped position back_base[s] + (i - recv_bounds[s])
+    back = [np.full(mat[s].sum(), -1, dtype=np.int64) for s in range(P)]
+    for d in range(P):
+        rb, bb = lays[d]["recv_bounds"], lays[d]["back_base"]
+        for s in range(P):
+            seg = recv[d][rb[s]:rb[s + 1]]
+            back[s][bb[s]:bb[s] + len(seg)] = seg
+    for s in range(P):
+        grouped = np.concatenate([rows[s][d] for d in range(P)])
+        assert np.array_equal(back[s], grouped)
+        assert lays[s]["n_send_max"] == mat.sum(axis=1).max()
