@@ -13,7 +13,7 @@ import threading
 from .errors import ConfigError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhashgraph_b200.so")
+LIB_PATH = os.environ.get("HG_LIB") or os.path.join(_HERE, "libhashgraph_b200.so")  # HG_LIB: experiment builds (tools/build_variant.py)
 
 HG_ERR_CONFIG = -1
 HG_ERR_CUDA = -2
