@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--load-factor", type=float, default=1.0)
     ap.add_argument("--key-bits", type=int, default=32, choices=[32, 64],
                     help="64: full SplitMix64 words as keys (BASELINE configs[3])")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-log2", type=int, default=24, help="CPU baseline sample size 2^x")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -357,25 +357,46 @@ def main():
         hq = torch.empty(q, dtype=sdt, pin_memory=True)
         hk.copy_(keys.cpu())
         hq.copy_(queries.cpu())
-        out = torch.empty(q, dtype=torch.int32, pin_memory=True)
+        # Two steps in flight on two streams (a serving loop): step i+1's H2D
+        # overlaps step i's kernels and D2H; PCIe is full duplex, so the step
+        # rate is bounded by the 2 GiB of inputs per step.  The host consumes
+        # every step's result (waits for its D2H, reads it) before reusing
+        # that step's output buffer.
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        outs = [torch.empty(q, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        done = [None, None]
+        checksum = 0
 
-        def e2e_step():
-            if use_dist:
-                table = hd.build_distributed(hk, cfg)
-                res = hd.query_distributed(table, hq)
-            else:
-                table = hg.build(hk, args.load_factor, key_bits=kb)
-                res = hg.intersect(table, hq)
-            out.copy_(res.multiplicities_device, non_blocking=True)
+        def e2e_step(i):
+            nonlocal checksum
+            slot = i % 2
+            if done[slot] is not None:
+                done[slot].synchronize()
+                checksum ^= int(outs[slot][0])  # the host reads the previous result of this slot
+            with torch.cuda.stream(streams[slot]):
+                if use_dist:
+                    table = hd.build_distributed(hk, cfg)
+                    res = hd.query_distributed(table, hq)
+                else:
+                    table = hg.build(hk, args.load_factor, key_bits=kb)
+                    res = hg.intersect(table, hq)
+                outs[slot].copy_(res.multiplicities_device, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                done[slot] = ev
             return res
 
-        e2e_step()
+        for i in range(2):
+            e2e_step(i)
         torch.cuda.synchronize()
+        done = [None, None]
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()
+        for i in range(args.e2e_steps):
+            e2e_step(i)
+            if os.environ.get("HG_E2E_TRACE"):
+                print(f"e2e step {i} enqueued at {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         if dist:
@@ -384,7 +405,8 @@ def main():
             e2e_s = float(t.item())
         e2e = {"value": (n + q) * world * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": (kb // 8) * (n + q), "d2h_bytes_per_step": 4 * q,
-               "ms_per_step": e2e_s / args.e2e_steps * 1e3}
+               "ms_per_step": e2e_s / args.e2e_steps * 1e3,
+               "pipeline": "2 steps in flight on 2 streams; host waits for and reads each result before reusing its buffer"}
 
     if rank != 0:
         if dist:
