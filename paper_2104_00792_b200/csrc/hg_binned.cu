@@ -1354,7 +1354,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 8
   BigMap<K>& map = *reinterpret_cast<BigMap<K>*>(reinterpret_cast<unsigned char*>(tedges) + (kCap + 8) * sizeof(K));
   const uint32_t f = blockIdx.x;
-  const uint32_t qlo = q_start[f], qhi = q_start[f + 1];
+  const uint32_t qlo = q_start[f];
+  uint32_t qhi = q_start[f + 1];
   if (qlo == qhi) return;
   K qv[kProbeQPT];
   load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
@@ -1454,6 +1455,9 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   __syncthreads();
   const bool overflow = map.full != 0;
   uint64_t matched = 0, total = 0, comps = 0;
+#if defined(HG_EXP_PROBE) && HG_EXP_PROBE == 3  // timing experiment (tools/build_variant.py): first batch only
+  qhi = min(qhi, qlo + kProbeQPT * kT);
+#endif
   if (in_smem)
     probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, mult_bo, qv, matched, total,
                           comps);
