@@ -366,16 +366,16 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
     if (s_h[f]) atomicAdd(fine_cnt + f, s_h[f]);
 }
 
-// Thread per level-1 bin: exclusive prefix down the CTA column (in place).
-__global__ void k_colscan(uint32_t* __restrict__ M, uint32_t G, uint32_t nb1) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nb1) return;
-  uint32_t run = 0;
-  for (uint32_t g = 0; g < G; g++) {
-    const uint32_t c = M[(uint64_t)g * nb1 + b];
-    M[(uint64_t)g * nb1 + b] = run;
-    run += c;
-  }
+// One CTA per level-1 bin: exclusive prefix down its column of per-CTA counts
+// (in place).  All G loads are in flight at once; a thread-per-bin serial walk
+// was 296 dependent loads long.
+__global__ void __launch_bounds__(1024) k_colscan(uint32_t* __restrict__ M, uint32_t G, uint32_t nb1) {
+  extern __shared__ uint32_t s_col[];  // G
+  const uint32_t b = blockIdx.x;
+  for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) s_col[g] = M[(uint64_t)g * nb1 + b];
+  __syncthreads();
+  block_exscan(s_col, G);
+  for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) M[(uint64_t)g * nb1 + b] = s_col[g];
 }
 
 // One CTA: fine starts (F+1), level-1 starts (nb1+1), level-2 tile prefix
@@ -396,7 +396,7 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
     if (t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
   }
   __syncthreads();
-  const uint32_t total = block_exscan(s_a, nfine);
+  const uint32_t total = block_exscan_rows(s_a, nfine, 0);  // warp-row layout: no bank conflicts
   for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
     fine_start[i] = s_a[i];
     fine_cursor[i] = s_a[i];
@@ -1546,7 +1546,8 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
   HG_LAUNCH("hg_hist", k_hist<H>, L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk, po->M,
             fine_cnt);
-  HG_LAUNCH("hg_colscan", k_colscan, (L.nb1 + 127) / 128, 128, 0, st, po->M, L.grid, L.nb1);
+  HG_LAUNCH("hg_colscan", k_colscan, L.nb1, (L.grid + 31) / 32 * 32 > 1024 ? 1024 : (L.grid + 31) / 32 * 32,
+            (size_t)L.grid * 4, st, po->M, L.grid, L.nb1);
   const size_t smS = ((size_t)L.nfine + L.nb1 + 1) * 4;
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smS));
   HG_LAUNCH("hg_starts", k_starts, 1, 1024, smS, st, fine_cnt, L.nfine, L.group, L.nb1, L.tile, cap, po->fine_start,
