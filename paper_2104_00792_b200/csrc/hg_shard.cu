@@ -315,7 +315,11 @@ k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
 // positional query merge do not need; the reference-order API
 // (hg_reorganize) keeps the stable two-pass kernels.  (Staging the tile in
 // smem to write one run per destination measured slower.)
-template <typename K, bool kPeer>
+//
+// MAXP > 0 (P <= MAXP, the GPU count of a node): ranks come from one ballot
+// per destination per round with warp-uniform running counts in registers --
+// no smem traffic or warp syncs per round; MAXP == 0 uses match_any.
+template <typename K, bool kPeer, int MAXP>
 __global__ void __launch_bounds__(kReorgWarps * 32)
 k_route_claim(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin, const long long* __restrict__ splits,
               uint32_t shards, const unsigned long long* __restrict__ row_offsets,
@@ -339,16 +343,43 @@ k_route_claim(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
   __syncthreads();
   uint32_t* my = s_wcnt + warp * shards;
   uint32_t dr[kReorgPerLane];  // destination << 16 | rank inside the warp's keys for it (or ~0)
+  if (MAXP > 0) {
+    uint32_t cnt[MAXP > 0 ? MAXP : 1];
 #pragma unroll
-  for (int r = 0; r < kReorgPerLane; r++) {
-    const bool ok = wbase + r * 32 + lane < n;
-    const uint32_t d = ok ? dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards) : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t cur = ok ? my[d] : 0u;
-    __syncwarp();
-    if (ok && (peers & lt) == 0) my[d] = cur + __popc(peers);
-    __syncwarp();
-    dr[r] = ok ? (d << 16) | (cur + __popc(peers & lt)) : 0xffffffffu;
+    for (int dd = 0; dd < MAXP; dd++) cnt[dd] = 0;
+#pragma unroll
+    for (int r = 0; r < kReorgPerLane; r++) {
+      const bool ok = wbase + r * 32 + lane < n;
+      const uint32_t d = ok ? (shards == 1 ? 0u : dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards))
+                            : 0xffffffffu;
+      uint32_t rank = 0;
+#pragma unroll
+      for (int dd = 0; dd < MAXP; dd++) {
+        if ((uint32_t)dd < shards) {
+          const uint32_t m = __ballot_sync(0xffffffffu, d == (uint32_t)dd);
+          if (d == (uint32_t)dd) rank = cnt[dd] + __popc(m & lt);
+          cnt[dd] += __popc(m);
+        }
+      }
+      dr[r] = ok ? (d << 16) | rank : 0xffffffffu;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int dd = 0; dd < MAXP; dd++)
+        if ((uint32_t)dd < shards) my[dd] = cnt[dd];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kReorgPerLane; r++) {
+      const bool ok = wbase + r * 32 + lane < n;
+      const uint32_t d = ok ? dest_of_bin(div_by(hash_mod(kv[r], hp), bin), s_splits, shards) : 0xffffffffu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t cur = ok ? my[d] : 0u;
+      __syncwarp();
+      if (ok && (peers & lt) == 0) my[d] = cur + __popc(peers);
+      __syncwarp();
+      dr[r] = ok ? (d << 16) | (cur + __popc(peers & lt)) : 0xffffffffu;
+    }
   }
   __syncthreads();
   for (uint32_t d = threadIdx.x; d < shards; d += blockDim.x) {
@@ -498,6 +529,26 @@ static int reorg_check(int key_bits, int kind, uint64_t hash_range, uint32_t sha
   return HG_OK;
 }
 
+// hg_route's launch: the ballot-ranked kernel sized to the shard count when
+// it is a node's GPU count (<= 8), the match_any kernel beyond.
+template <typename K, bool kPeer>
+static int route_launch(const K* keys, uint64_t n, const HashParams& hp, const DivParams& dp, const long long* sp,
+                        uint32_t shards, const unsigned long long* ro, const unsigned long long* dpt,
+                        const unsigned long long* db, K* grouped, uint32_t* order, unsigned long long* cur,
+                        uint64_t tiles, size_t smem, cudaStream_t s) {
+  auto go = [&](auto kern) -> int {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HG_LAUNCH("hg_route", kern, (unsigned)tiles, kReorgWarps * 32, smem, s, keys, n, hp, dp, sp, shards, ro, dpt, db,
+              grouped, order, cur);
+    return HG_OK;
+  };
+  if (shards == 1) return go(k_route_claim<K, kPeer, 1>);
+  if (shards == 2) return go(k_route_claim<K, kPeer, 2>);
+  if (shards <= 4) return go(k_route_claim<K, kPeer, 4>);
+  if (shards <= 8) return go(k_route_claim<K, kPeer, 8>);
+  return go(k_route_claim<K, kPeer, 0>);
+}
+
 }  // namespace hg
 
 using namespace hg;
@@ -634,25 +685,11 @@ int hg_route(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed
   auto* cur = (unsigned long long*)cursors;
   const auto* sp = (const long long*)splits;
   if (key_bits == 32) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (peer)
-      HG_LAUNCH("hg_route", (k_route_claim<uint32_t, true>), (unsigned)tiles, kReorgWarps * 32, smem, s,
-                (const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur);
-    else
-      HG_LAUNCH("hg_route", (k_route_claim<uint32_t, false>), (unsigned)tiles, kReorgWarps * 32, smem, s,
-                (const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur);
-  } else {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_route_claim<uint64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (peer)
-      HG_LAUNCH("hg_route", (k_route_claim<uint64_t, true>), (unsigned)tiles, kReorgWarps * 32, smem, s,
-                (const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur);
-    else
-      HG_LAUNCH("hg_route", (k_route_claim<uint64_t, false>), (unsigned)tiles, kReorgWarps * 32, smem, s,
-                (const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur);
+    if (peer) return route_launch<uint32_t, true>((const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur, tiles, smem, s);
+    return route_launch<uint32_t, false>((const uint32_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint32_t*)grouped, order, cur, tiles, smem, s);
   }
-  return HG_OK;
+  if (peer) return route_launch<uint64_t, true>((const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur, tiles, smem, s);
+  return route_launch<uint64_t, false>((const uint64_t*)keys, n, hp, dp, sp, shards, ro, dpt, db, (uint64_t*)grouped, order, cur, tiles, smem, s);
 }
 
 int hg_return_peers(const uint32_t* vals, uint64_t n, const uint64_t* recv_bounds, const uint64_t* back_ptrs,
