@@ -1165,7 +1165,10 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
   }
 }
 
-constexpr int kProbeQPT = 16;  // queries per thread per probe batch
+#ifndef HG_PROBE_QPT
+#define HG_PROBE_QPT 8
+#endif
+constexpr int kProbeQPT = HG_PROBE_QPT;  // queries per thread per probe batch (the next batch is prefetched)
 
 template <typename K>
 __device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qhi, K (&qv)[kProbeQPT]) {
@@ -1286,8 +1289,13 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
                                                    uint64_t& matched, uint64_t& total, uint64_t& comps) {
   using K = typename H::Key;
   constexpr int QPT = kProbeQPT;
+  K qn[QPT];  // the next batch, in flight while this one is probed
   for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
-    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);  // the first batch was loaded before staging
+    if (q0 != qlo) {
+#pragma unroll
+      for (int k = 0; k < QPT; k++) qv[k] = qn[k];  // (the first batch was loaded before staging)
+    }
+    if (q0 + QPT * kT < qhi) load_queries<K>(qpart, q0 + QPT * kT, qhi, qn);
     const uint32_t kmax = (qhi - q0 + kT - 1) / kT;       // query slots this batch fills (CTA-uniform)
     uint32_t ae[QPT];
     bool deep = false;
