@@ -768,23 +768,32 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       tix = t;
     }
   };
-  // run offsets + global bases of tile i into buffer bf; level-1 bases chain
-  // from the previous tile (buffer bf ^ 1)
-  auto load_meta = [&](uint32_t i, int bf) {
-    uint64_t t0, tix;
-    uint32_t m;
-    tile_of(i, t0, m, tix);
+  // Per tile, thread x <= nbb holds its meta words in registers one tile
+  // ahead: level 1 the run offset toff[x]; level 2 the claim base[x] and
+  // toff[x].  They are loaded from global memory while the previous tile is
+  // gathered and only stored to smem (no global latency) before the barrier.
+  auto meta_load = [&](uint64_t tix, uint32_t& r0, uint32_t& r1) {
+    const uint32_t x = threadIdx.x;
     if (kLevel == 1) {
-      for (uint32_t x = threadIdx.x; x <= nb; x += blockDim.x) toff[bf * TO + x] = meta[tix * (nb + 1) + x];
-      if (threadIdx.x < nb) {
-        const uint32_t b = threadIdx.x, pb = (bf ^ 1) * TO;
-        base[bf * kMaxBins + b] = i == 0 ? c_start[b] + M[(uint64_t)blockIdx.x * nb + b]
-                                         : base[(bf ^ 1) * kMaxBins + b] + toff[pb + b + 1] - toff[pb + b];
+      if (x <= nb) r0 = meta[tix * (nb + 1) + x];
+    } else {
+      if (x < kSub) r1 = meta[tix * (2 * kSub + 1) + x];
+      if (x <= kSub) r0 = meta[tix * (2 * kSub + 1) + kSub + x];
+    }
+  };
+  // registers -> buffer bf; level-1 bases chain from the previous tile (bf ^ 1)
+  auto meta_store = [&](uint32_t i, int bf, uint32_t r0, uint32_t r1) {
+    const uint32_t x = threadIdx.x;
+    if (kLevel == 1) {
+      if (x <= nb) toff[bf * TO + x] = r0;
+      if (x < nb) {
+        const uint32_t pb = (bf ^ 1) * TO;
+        base[bf * kMaxBins + x] = i == 0 ? c_start[x] + M[(uint64_t)blockIdx.x * nb + x]
+                                         : base[(bf ^ 1) * kMaxBins + x] + toff[pb + x + 1] - toff[pb + x];
       }
     } else {
-      for (uint32_t x = threadIdx.x; x < kSub; x += blockDim.x) base[bf * kMaxBins + x] = meta[tix * (2 * kSub + 1) + x];
-      for (uint32_t x = threadIdx.x; x <= kSub; x += blockDim.x)
-        toff[bf * TO + x] = meta[tix * (2 * kSub + 1) + kSub + x];
+      if (x < kSub) base[bf * kMaxBins + x] = r1;
+      if (x <= kSub) toff[bf * TO + x] = r0;
     }
   };
   // one thread per bin: aligned body by TMA, < 4-element head/tail by hand
@@ -807,41 +816,53 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       }
     }
   };
-  load_meta(0, 0);
+  uint64_t t0c, t0n = 0, tix;
+  uint32_t mc, mn = 0;
+  uint32_t r0 = 0, r1 = 0;  // meta of the next tile (it + 1), in flight
+  tile_of(0, t0c, mc, tix);
+  meta_load(tix, r0, r1);
+  meta_store(0, 0, r0, r1);
   __syncthreads();
   issue(0);
   __syncthreads();
   if (threadIdx.x == 0) mbar_arrive(bar);
+  if (ntiles > 1) {
+    tile_of(1, t0n, mn, tix);
+    meta_load(tix, r0, r1);
+  }
   for (uint32_t it = 0; it < ntiles; it++) {
     const int cur = it & 1, nxt = cur ^ 1;
     const bool more = it + 1 < ntiles;
-    uint64_t t0, tix;
-    uint32_t m;
-    tile_of(it, t0, m, tix);
     const uint32_t* st = staged + cur * kUnpStaged;
-    const bool vec = kLevel == 1 && m == tile && tile == (uint32_t)VPT * kT;
+    const bool vec = kLevel == 1 && mc == tile && tile == (uint32_t)VPT * kT;
     // position maps of tile it load while tile it+1's runs are requested
     uint4 pm4[VPT / 8];
     uint32_t pm[VPT];
     if (vec) {
-      const uint4* p4 = reinterpret_cast<const uint4*>(pmap + t0);
+      const uint4* p4 = reinterpret_cast<const uint4*>(pmap + t0c);
 #pragma unroll
       for (int k = 0; k < VPT / 8; k++) pm4[k] = p4[k * kT + threadIdx.x];
     } else {
 #pragma unroll
       for (int k = 0; k < VPT; k++) {
         const uint32_t i = k * kT + threadIdx.x;
-        pm[k] = i < m ? pmap[t0 + i] : 0u;
+        pm[k] = i < mc ? pmap[t0c + i] : 0u;
       }
     }
-    if (more) load_meta(it + 1, nxt);
+    if (more) meta_store(it + 1, nxt, r0, r1);
     __syncthreads();
     if (more) issue(nxt);
+    uint64_t t0nn = 0;
+    uint32_t mnn = 0;
+    if (it + 2 < ntiles) {  // look ahead: tile it+2's position and meta load during this gather
+      tile_of(it + 2, t0nn, mnn, tix);
+      meta_load(tix, r0, r1);
+    }
     mbar_wait(bar + cur, (it >> 1) & 1);
     if (vec) {
       // full level-1 tiles are 16-byte aligned: 8 slots per 16-byte load,
       // 4 values per 16-byte store
-      uint4* o4 = reinterpret_cast<uint4*>(out + t0);
+      uint4* o4 = reinterpret_cast<uint4*>(out + t0c);
 #pragma unroll
       for (int k = 0; k < VPT / 8; k++) {
         const uint32_t w[4] = {pm4[k].x, pm4[k].y, pm4[k].z, pm4[k].w};
@@ -853,12 +874,16 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
 #pragma unroll
       for (int k = 0; k < VPT; k++) {
         const uint32_t i = k * kT + threadIdx.x;
-        if (i < m) out[t0 + i] = st[pm[k]];
+        if (i < mc) out[t0c + i] = st[pm[k]];
       }
     }
     fence_proxy_async();  // generic reads of this buffer before the next bulk writes into it
     __syncthreads();      // buffer cur free; tile it+1's expect_tx all posted
     if (more && threadIdx.x == 0) mbar_arrive(bar + nxt);
+    t0c = t0n;
+    mc = mn;
+    t0n = t0nn;
+    mn = mnn;
   }
 }
 
