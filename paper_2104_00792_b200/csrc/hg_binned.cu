@@ -642,30 +642,31 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
   }
   __syncthreads();
   const uint32_t ntiles = s.tp[nb1];
-  auto locate = [&](uint32_t t, uint32_t& c, uint32_t& t0, uint32_t& m) {
+  // thread 0 locates a tile (binary search over the level-2 tile prefix plus
+  // two c_start loads) when it issues the tile's TMA, one tile ahead, and
+  // leaves (bin, first element, size) in smem: no global latency at the top
+  // of a tile
+  __shared__ uint32_t s_loc[3];
+  auto locate_issue = [&](uint32_t t) {
     uint32_t a = 0, z = nb1;  // level-1 bin c: tp[c] <= t < tp[c+1]
     while (z - a > 1) {
       const uint32_t mid = (a + z) >> 1;
       if (s.tp[mid] <= t) a = mid; else z = mid;
     }
-    c = a;
-    t0 = c_start[c] + (t - s.tp[c]) * TS::kTile;
-    m = min((uint32_t)TS::kTile, c_start[c + 1] - t0);
-  };
-  auto issue = [&](uint32_t t0, uint32_t m) {
+    const uint32_t t0 = c_start[a] + (t - s.tp[a]) * TS::kTile;
+    const uint32_t m = min((uint32_t)TS::kTile, c_start[a + 1] - t0);
+    s_loc[0] = a;
+    s_loc[1] = t0;
+    s_loc[2] = m;
     const uint32_t a0 = t0 & ~(VPL - 1);
     const uint32_t bytes = ((t0 - a0 + m) * (uint32_t)sizeof(K) + 15) & ~15u;
     tma_load_1d(s.raw, in + a0, bytes, &s.bar);
   };
   uint32_t parity = 0;
-  if (threadIdx.x == 0 && blockIdx.x < ntiles) {
-    uint32_t c, t0, m;
-    locate(blockIdx.x, c, t0, m);
-    issue(t0, m);
-  }
+  if (threadIdx.x == 0 && blockIdx.x < ntiles) locate_issue(blockIdx.x);
+  __syncthreads();  // s_loc of the first tile (later ones are ordered by the tile loop's barriers)
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    uint32_t c, t0, m;
-    locate(t, c, t0, m);
+    const uint32_t c = s_loc[0], t0 = s_loc[1], m = s_loc[2];
     mbar_wait(&s.bar, parity);
     parity ^= 1;
     const uint32_t sh = t0 & (VPL - 1);
@@ -684,12 +685,8 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     }
     if (threadIdx.x < kSub) tma_store_wait_read();
     fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0 && t + gridDim.x < ntiles) {
-      uint32_t c2, t02, m2;
-      locate(t + gridDim.x, c2, t02, m2);
-      issue(t02, m2);
-    }
+    __syncthreads();  // raw and s_loc consumed by every thread
+    if (threadIdx.x == 0 && t + gridDim.x < ntiles) locate_issue(t + gridDim.x);
     uint32_t rk[KPT / 2];
     rank_tile<K, KPT, false>(s, bp, rk, m, kSub);
     if (threadIdx.x < kSub) {
