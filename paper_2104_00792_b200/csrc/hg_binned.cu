@@ -422,13 +422,19 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
 
 // Runs are staged in smem at positions congruent (mod 4 elements) to their
 // global destination, so the aligned body of every run leaves with one TMA
-// bulk store: bin b's run starts at pt[b] = toff[b] + 4b + ((dst[b] - toff[b]) & 3).
-constexpr uint32_t kPadMod = 4;
+// bulk store: bin b's run starts at pt[b] = toff[b] + 8b + 4 + ((dst[b] - toff[b]) & 3).
+// The 5..11 slots between runs also leave room for the 16-byte-aligned
+// superset of every run (<= 3 slots either side, never overlapping the next
+// run's superset), so the unpartition pulls each run back with one bulk copy
+// and no per-element head/tail loads.
+constexpr uint32_t kPadMod = 4;                  // alignment unit (elements)
+constexpr uint32_t kPadRun = 8;                  // staged slots reserved per bin
+constexpr uint32_t kPadTotal = kPadRun * kMaxBins + 2 * kPadMod;  // staged size over the tile
 
 template <typename K>
 struct PartSmem {
   K raw[TileShape<K>::kTile + 16 / sizeof(K)];              // TMA landing buffer (next tile)
-  K staged[TileShape<K>::kTile + kPadMod * kMaxBins + 2 * kPadMod];  // runs, padded for alignment
+  K staged[TileShape<K>::kTile + kPadTotal];  // runs, padded for alignment
   uint32_t wcnt[kW][kMaxBins];  // per-warp counts -> per-warp slot bases
   uint32_t toff[kMaxBins + 1];  // tile offsets per bin (unpadded)
   uint32_t pt[kMaxBins];        // padded staged start per bin
@@ -438,7 +444,7 @@ struct PartSmem {
 };
 
 __device__ __forceinline__ uint32_t pad_start(uint32_t toff, uint32_t b, uint32_t dst) {
-  return toff + kPadMod * b + ((dst - toff) & (kPadMod - 1));
+  return toff + kPadRun * b + kPadMod + ((dst - toff) & (kPadMod - 1));
 }
 
 // Rank a register tile by bin: one atomic on the warp's private bin counter
@@ -711,7 +717,7 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
 // pulled back into its padded staged slot range (TMA for the aligned body),
 // then out[i] = staged[pmap[i]].  Two staging buffers: tile i+1's runs are in
 // flight (meta read, bulk loads issued) while tile i is gathered.
-constexpr uint32_t kUnpStaged = 8192 + kPadMod * kMaxBins + 2 * kPadMod;
+constexpr uint32_t kUnpStaged = 8192 + kPadTotal;
 
 template <int kLevel>
 __global__ void __launch_bounds__(kT, 2)
@@ -793,7 +799,9 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       if (x <= kSub) toff[bf * TO + x] = r0;
     }
   };
-  // one thread per bin: aligned body by TMA, < 4-element head/tail by hand
+  // one thread per bin: the run's 16-byte-aligned superset in one bulk copy
+  // (the padding absorbs the <= 3 extra slots on each side; `vals` carries
+  // 16 bytes of tail padding)
   auto issue = [&](int bf) {
     if (threadIdx.x < nbb) {
       const uint32_t b = threadIdx.x;
@@ -802,14 +810,9 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
         uint32_t* st = staged + bf * kUnpStaged;
         const uint32_t g = base[bf * kMaxBins + b];
         const uint32_t p = pad_start(toff[bf * TO + b], b, g);
-        const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
-        const uint32_t body = (cnt - h) & ~(kPadMod - 1);
-        if (body) {
-          mbar_expect_tx(bar + bf, body * 4);
-          tma_load_1d_tx(st + p + h, vals + g + h, body * 4, bar + bf);
-        }
-        for (uint32_t i = 0; i < h; i++) st[p + i] = vals[g + i];
-        for (uint32_t i = h + body; i < cnt; i++) st[p + i] = vals[g + i];
+        const uint32_t g0 = g & ~(kPadMod - 1), g1 = (g + cnt + kPadMod - 1) & ~(kPadMod - 1);
+        mbar_expect_tx(bar + bf, (g1 - g0) * 4);
+        tma_load_1d_tx(st + p - (g - g0), vals + g0, (g1 - g0) * 4, bar + bf);
       }
     }
   };
@@ -1520,7 +1523,7 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query)
     b += 2 * align_up(n * 2, 256);                       // pmap1, pmap2
     b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
     b += align_up(L.max_tiles2 * (2 * kSub + 1) * 4, 256);  // meta2
-    b += align_up(n * 4, 256);                           // bin-ordered multiplicities
+    b += align_up(n * 4 + 16, 256);                      // bin-ordered multiplicities (+ tail padding)
   } else {
     b += align_up((size_t)num_sms() * (1u << L.s) * 4, 256);  // big-bin scratch
   }
@@ -1640,7 +1643,7 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyO
   PartOut po{};
   int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
   if (rc) return rc;
-  uint32_t* mult_bo = ws.take<uint32_t>(q);
+  uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
