@@ -992,21 +992,23 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     while (f < nfine && fine_start[f + 1] - fine_start[f] > kCap) f += gridDim.x;
     return f;
   };
-  // bin f's keys [lo, hi) land at raw[lo - lo_al ...]: the 16-byte aligned
-  // part by TMA (thread 0), the < VPL keys after the last boundary by threads
-  // 0..VPL-1 (nothing past hi is read)
+  // bin f's keys [lo, hi) land at raw[lo - lo_al ...] with one bulk copy of
+  // their 16-byte-aligned superset (the few keys of the neighbouring bins it
+  // brings along are never read).  Only the array's last bin, whose superset
+  // would run past the end, copies the aligned part and loads the < VPL keys
+  // after it by threads 0..VPL-1.
   auto fetch = [&](uint32_t f) {
+    if (threadIdx.x >= VPL) return;  // threads 0..VPL-1 only: short-lived registers
     const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
-    const uint32_t lo_al = lo & ~(VPL - 1), hi_al = hi & ~(VPL - 1);
+    const uint32_t lo_al = lo & ~(VPL - 1), hi_up = (hi + VPL - 1) & ~(VPL - 1);
+    const uint32_t hi_cp = hi_up <= fine_start[nfine] ? hi_up : hi & ~(VPL - 1);
     if (threadIdx.x == 0) {
-      const uint32_t bytes = hi_al > lo_al ? (hi_al - lo_al) * (uint32_t)sizeof(K) : 0u;
+      const uint32_t bytes = hi_cp > lo_al ? (hi_cp - lo_al) * (uint32_t)sizeof(K) : 0u;
       if (bytes) tma_load_1d(raw, src + lo_al, bytes, &s_bar);
       else mbar_arrive(&s_bar);
     }
-    if (threadIdx.x < VPL) {
-      const uint32_t g = hi_al + threadIdx.x;
-      if (g >= lo && g < hi) raw[g - lo_al] = src[g];
-    }
+    const uint32_t g = hi_cp + threadIdx.x;
+    if (g >= lo && g < hi) raw[g - lo_al] = src[g];
   };
   uint32_t f = next_small(blockIdx.x);
   if (threadIdx.x == 0) {
