@@ -1045,28 +1045,36 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     if (fn < nfine) fetch(fn);
     // count: the atomic's old value is the key's rank inside its bucket.
     // Only the first and last chunk of a bin can be partial, so validity is
-    // decided per chunk and full chunks run branch-free.
-    uint32_t pk[CPT * VPL];
-    auto count_key = [&](K key) -> uint32_t {
+    // decided per chunk and full chunks run branch-free.  u32 keys keep only
+    // the rank (packed u16, two per register) and re-hash the bucket at
+    // placement: 20 keys per thread plus (bucket, rank) words spilled at 64
+    // registers; u64 keys (10 per thread) keep (bucket << 16 | rank) -- their
+    // re-hash (fmix64) costs more than it saves.
+    constexpr bool kRehash = sizeof(K) == 4;
+    constexpr int NK = CPT * (int)VPL;
+    constexpr int NW = kRehash ? (NK + 1) / 2 : NK;  // rank words
+    uint32_t rk[NW];
+#pragma unroll
+    for (int i = 0; i < NW; i++) rk[i] = 0;
+    auto count_key = [&](K key, int k) {
       const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
       const uint32_t sft = (l & 1) * 16;
-      const uint32_t old = atomicAdd(c16 + (l >> 1), 1u << sft);
-      return (l << 16) | ((old >> sft) & 0xFFFFu);
+      const uint32_t r = (atomicAdd(c16 + (l >> 1), 1u << sft) >> sft) & 0xFFFFu;
+      if (kRehash) rk[k >> 1] |= r << ((k & 1) * 16);
+      else rk[k] = (l << 16) | r;
     };
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
       const uint32_t c = i * NT + threadIdx.x;
       const uint32_t e0 = c * VPL;
-#pragma unroll
-      for (int j = 0; j < (int)VPL; j++) pk[i * VPL + j] = 0xFFFFFFFFu;
       if (c < nch) {
         if (e0 >= sh && e0 + VPL <= sh + cnt) {
 #pragma unroll
-          for (int j = 0; j < (int)VPL; j++) pk[i * VPL + j] = count_key(kv[i * VPL + j]);
+          for (int j = 0; j < (int)VPL; j++) count_key(kv[i * VPL + j], i * VPL + j);
         } else {
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
-            if (e0 + j - sh < cnt) pk[i * VPL + j] = count_key(kv[i * VPL + j]);
+            if (e0 + j - sh < cnt) count_key(kv[i * VPL + j], i * VPL + j);
         }
       }
     }
@@ -1075,14 +1083,26 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
     __syncthreads();
     K* stg = staged + sh;
+    auto place_key = [&](K key, int k) {
+      if (kRehash) {
+        const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
+        stg[get16(c16, l) + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu)] = key;
+      } else {
+        stg[get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu)] = key;
+      }
+    };
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
       const uint32_t c = i * NT + threadIdx.x;
+      const uint32_t e0 = c * VPL;
       if (c < nch) {
+        if (e0 >= sh && e0 + VPL <= sh + cnt) {
 #pragma unroll
-        for (int j = 0; j < (int)VPL; j++) {
-          const uint32_t p = pk[i * VPL + j];
-          if (p != 0xFFFFFFFFu) stg[get16(c16, p >> 16) + (p & 0xFFFFu)] = kv[i * VPL + j];
+          for (int j = 0; j < (int)VPL; j++) place_key(kv[i * VPL + j], i * VPL + j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < (int)VPL; j++)
+            if (e0 + j - sh < cnt) place_key(kv[i * VPL + j], i * VPL + j);
         }
       }
     }
