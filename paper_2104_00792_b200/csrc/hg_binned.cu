@@ -1328,60 +1328,80 @@ __device__ __forceinline__ void probe_queries_global(const KeyOf<H>* __restrict_
 // almost every warp), so the rest runs as a warp-uniform loop to the warp's
 // deepest bucket rather than a divergent per-lane loop.  Buckets deeper than
 // kBigDeg are answered from the map (one warp-uniform check per batch).
+// One batch (QPT queries per thread): kFull -- every query slot of the batch
+// is valid, so no bounds checks; bin_deep -- the bin has buckets deeper than
+// kBigDeg (known from staging), only then are queries checked for the map.
+template <typename H, bool kFull>
+__device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const HashParams& hp, uint32_t first,
+                                            const uint16_t* off16, const KeyOf<H>* te, const BigMap<KeyOf<H>>& map,
+                                            bool overflow, bool bin_deep, uint32_t* __restrict__ mult_bo,
+                                            const KeyOf<H> (&qv)[kProbeQPT], uint32_t& m32, uint32_t& t32,
+                                            uint32_t& d32) {
+  using K = typename H::Key;
+  constexpr int QPT = kProbeQPT;
+  const uint32_t kmax = kFull ? (uint32_t)QPT : (qhi - q0 + kT - 1) / kT;  // query slots this batch fills
+  uint32_t ae[QPT];
+#pragma unroll
+  for (int k = 0; k < QPT; k++) {
+    ae[k] = 0;
+    if (!kFull && (uint32_t)k >= kmax) continue;
+    if (kFull || q0 + k * kT + threadIdx.x < qhi) {
+      const uint32_t l = H::bucket(qv[k], hp) - first;
+      ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
+    }
+  }
+  bool deep = false;
+  if (bin_deep) {
+#pragma unroll
+    for (int k = 0; k < QPT; k++) deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
+  }
+  const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
+#pragma unroll
+  for (int k = 0; k < QPT; k++) {
+    if (!kFull && (uint32_t)k >= kmax) break;
+    const K q = qv[k];
+    const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
+    const bool mapped = use_map && d > kBigDeg;
+    const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
+    uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
+                 (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped ? 0u : d);
+    for (uint32_t t = 4; t < dmax; t++) {
+      const bool in = t < d;
+      const K x = in ? te[a + t] : K(0);
+      c += (uint32_t)(in & (x == q));
+    }
+    if (use_map && mapped) c = map_count(map, q);
+    const uint32_t j = q0 + k * kT + threadIdx.x;
+    if (kFull || j < qhi) {
+      mult_bo[j] = c;
+      m32 += (c != 0);
+      t32 += c;
+      d32 += d;
+    }
+  }
+}
+
 template <typename H>
 __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
                                                    const HashParams& hp, uint32_t first, const uint16_t* off16,
                                                    const KeyOf<H>* te, const BigMap<KeyOf<H>>& map, bool overflow,
-                                                   uint32_t* __restrict__ mult_bo, KeyOf<H> (&qv)[kProbeQPT],
-                                                   uint64_t& matched, uint64_t& total, uint64_t& comps) {
+                                                   bool bin_deep, uint32_t* __restrict__ mult_bo,
+                                                   KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
+                                                   uint64_t& comps) {
   using K = typename H::Key;
   constexpr int QPT = kProbeQPT;
+  constexpr uint32_t B = QPT * kT;
   K qn[QPT];  // the next batch, in flight while this one is probed
-  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += B) {
     if (q0 != qlo) {
 #pragma unroll
       for (int k = 0; k < QPT; k++) qv[k] = qn[k];  // (the first batch was loaded before staging)
     }
-    if (q0 + QPT * kT < qhi) load_queries<K>(qpart, q0 + QPT * kT, qhi, qn);
-    const uint32_t kmax = (qhi - q0 + kT - 1) / kT;       // query slots this batch fills (CTA-uniform)
-    uint32_t ae[QPT];
-    bool deep = false;
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      ae[k] = 0;
-      if ((uint32_t)k >= kmax) continue;
-      if (q0 + k * kT + threadIdx.x < qhi) {
-        const uint32_t l = H::bucket(qv[k], hp) - first;
-        ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
-        deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
-      }
-    }
-    const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
+    if (q0 + B < qhi) load_queries<K>(qpart, q0 + B, qhi, qn);
     uint32_t m32 = 0, t32 = 0, d32 = 0;
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      if ((uint32_t)k >= kmax) break;
-      const K q = qv[k];
-      const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
-      const bool mapped = use_map && d > kBigDeg;
-      const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
-      uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
-                   (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
-      const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped ? 0u : d);
-      for (uint32_t t = 4; t < dmax; t++) {
-        const bool in = t < d;
-        const K x = in ? te[a + t] : K(0);
-        c += (uint32_t)(in & (x == q));
-      }
-      if (use_map && mapped) c = map_count(map, q);
-      const uint32_t j = q0 + k * kT + threadIdx.x;
-      if (j < qhi) {
-        mult_bo[j] = c;
-        m32 += (c != 0);
-        t32 += c;
-        d32 += d;
-      }
-    }
+    if (qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_deep, mult_bo, qv, m32, t32, d32);
+    else probe_batch<H, false>(q0, qhi, hp, first, off16, te, map, overflow, bin_deep, mult_bo, qv, m32, t32, d32);
     matched += m32;
     total += t32;
     comps += d32;
@@ -1514,8 +1534,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   qhi = min(qhi, qlo + kProbeQPT * kT);
 #endif
   if (in_smem)
-    probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, mult_bo, qv, matched, total,
-                          comps);
+    probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, s_deep != 0, mult_bo, qv,
+                          matched, total, comps);
   else
     probe_queries_global<H>(qpart, qlo, qhi, hp, t_off, t_edges, map, overflow, mult_bo, qv, matched, total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
