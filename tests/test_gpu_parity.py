@@ -237,3 +237,22 @@ def test_high_duplicate_build_and_query(n, values, lf):
     assert np.array_equal(res.multiplicities, O.count_occurrences(keys, queries))
     _, matched, total, comp, _ = O.query(off, placed, queries)
     assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
+
+
+def test_c1_exact_vs_oracle():
+    """BASELINE C1 at full size (2^24 uint32 keys and 2^24 queries from the
+    reference's SplitMix64 streams, C = 1), bit-exact against the CPU
+    restatement: offsets equal, every bucket the same multiset, every
+    multiplicity and aggregate counter equal."""
+    spec = hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, 24, 1 << 24, 0)
+    keys = O.generate_keys(24, 1 << 24, 0)
+    queries = O.generate_keys(24, 1 << 24, 0x51)
+    assert np.array_equal(hg.generate(spec), keys)
+    table = hg.build(keys)
+    off, placed, _ = O.build_csr(keys, table.hash_range)
+    assert_table_equal(table, off, placed)
+    res = hg.intersect(table, queries)
+    mult, matched, total, comp, _ = O.query(off, placed, queries)
+    assert np.array_equal(res.multiplicities, mult)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
+    assert matched == 10_601_263  # SURVEY §8(d), measured with the reference
