@@ -205,6 +205,27 @@ class PeerBuffers:
     def __init__(self, group=None):
         self.group = group
         self._bufs = {}
+        self._ok = None
+
+    def available(self) -> bool:
+        """Whether symmetric memory works on every rank (decided once, agreed by
+        an all_reduce MIN so no rank takes the peer path alone)."""
+        if self._ok is None:
+            import warnings
+
+            import torch.distributed as dist
+
+            t = D.torch()
+            try:
+                self.get("probe", 1 << 10, t.int32)
+                ok = 1
+            except Exception as e:  # no symmetric-memory support: NCCL alltoallv instead
+                warnings.warn(f"peer-memory exchange unavailable ({e}); using NCCL all_to_all")
+                ok = 0
+            flag = t.tensor([ok], dtype=t.int32, device=D.device())
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            self._ok = bool(int(flag.item()))
+        return self._ok
 
     def get(self, name: str, n: int, dtype):
         import torch.distributed as dist
@@ -283,7 +304,7 @@ def build_distributed(local_keys, config: DistConfig = DistConfig(), group=None,
     n_recv = lay["n_recv"]
     row_off = np.concatenate([[0], np.cumsum(mat[rank])[:-1]])
     t2 = time.perf_counter_ns()
-    if config.transport == "p2p":
+    if config.transport == "p2p" and _peer_buffers(group).available():
         buf, handle, ptrs = _peer_buffers(group).get("keys", lay["capacity"], keys.dtype)
         handle.barrier()  # every rank is done reading its buffer from the previous exchange
         ops.route(keys, hr, bin_size, splits, world, config.family, row_off, ptrs, _dev_i64(ops, lay["dest_base"]))
@@ -327,7 +348,7 @@ def query_distributed(table: DistTable, local_queries, group=None, ops=None):
     mat = _gather_counts(dist, ops, ops.segment_sums(local_counts, splits), world, group)
     lay = peer_layout(mat, rank)
     row_off = np.concatenate([[0], np.cumsum(mat[rank])[:-1]])
-    if getattr(table, "transport", "nccl") == "p2p":
+    if getattr(table, "transport", "nccl") == "p2p" and _peer_buffers(group).available():
         pb = _peer_buffers(group)
         qbuf, handle, qptrs = pb.get("queries", lay["capacity"], q.dtype)
         bbuf, _, bptrs = pb.get("answers", lay["n_send_max"], t.int32)
