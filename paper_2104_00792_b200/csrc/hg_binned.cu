@@ -451,9 +451,13 @@ __device__ __forceinline__ uint32_t pad_start(uint32_t toff, uint32_t b, uint32_
 // per key (rank kept in registers), then a per-bin prefix over warps.  On
 // return s.wcnt[w][b] is warp w's offset inside bin b's run and s.toff the
 // tile offsets (s.toff[nb] = tile size).
+//
+// claims != nullptr (level 2): each bin's space is claimed (atomicAdd on
+// claims[b]) as soon as the bin's total is known, and the answer lands in
+// s.dst[b] after the bin scan, so the atomic's latency overlaps the scan.
 template <typename K, int KPT, bool kFull>
 __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[KPT / 4], uint32_t (&rk)[KPT / 2],
-                                          uint32_t m, uint32_t nb) {
+                                          uint32_t m, uint32_t nb, uint32_t* __restrict__ claims = nullptr) {
   constexpr bool vec = kFull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t b = lane; b < nb; b += 32) s.wcnt[warp][b] = 0;
@@ -466,6 +470,7 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
     if (k & 1) rk[k >> 1] |= r << 16; else rk[k >> 1] = r;
   }
   __syncthreads();
+  uint32_t d = 0;
   if (threadIdx.x < nb) {
     uint32_t run = 0;
 #pragma unroll
@@ -475,10 +480,12 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
       run += c;
     }
     s.toff[threadIdx.x] = run;
+    if (claims && run) d = atomicAdd(claims + threadIdx.x, run);
   }
   __syncthreads();
   const uint32_t total = block_exscan(s.toff, nb);
   if (threadIdx.x == 0) s.toff[nb] = total;
+  if (claims && threadIdx.x < nb) s.dst[threadIdx.x] = d;
   __syncthreads();
 }
 
@@ -694,16 +701,11 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     __syncthreads();  // raw and s_loc consumed by every thread
     if (threadIdx.x == 0 && t + gridDim.x < ntiles) locate_issue(t + gridDim.x);
     uint32_t rk[KPT / 2];
-    rank_tile<K, KPT, false>(s, bp, rk, m, kSub);
-    if (threadIdx.x < kSub) {
-      const uint32_t cnt = s.toff[threadIdx.x + 1] - s.toff[threadIdx.x];
-      const uint32_t d = cnt ? atomicAdd(fine_cursor + c * kSub + threadIdx.x, cnt) : 0u;
-      s.dst[threadIdx.x] = d;
-      if (kQuery) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = d;
-    }
-    if (kQuery)
+    rank_tile<K, KPT, false>(s, bp, rk, m, kSub, fine_cursor + c * kSub);
+    if (kQuery) {
+      if (threadIdx.x < kSub) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
-    __syncthreads();
+    }
     pad_bases(s.pt, s.wcnt, s.toff, s.dst, kSub);
     place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     store_runs<K>(s, kSub, out);
