@@ -1042,7 +1042,8 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
 #pragma unroll
       for (int j = 0; j < (int)VPL; j++) kv[i * VPL + j] = qk[j];
     }
-    for (uint32_t i = threadIdx.x; i < (nb + 1) / 2; i += NT) c16[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ((nb + 1) / 2 + 3) / 4; i += NT)  // 16-byte stores (c16 is 128-byte padded)
+      reinterpret_cast<uint4*>(c16)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();  // raw consumed, counters zero
     if (fn < nfine) fetch(fn);
     // count: the atomic's old value is the key's rank inside its bucket.
