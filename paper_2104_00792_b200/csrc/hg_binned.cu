@@ -309,12 +309,13 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
     const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
     const uint64_t nv = (hi - lo) / 2;
     uint64_t i = threadIdx.x;
-    for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
-      uint4 q[4];
+    constexpr int U = 8;  // 16-byte loads in flight per thread (two keys each)
+    for (; i + (U - 1) * blockDim.x < nv; i += U * blockDim.x) {
+      uint4 q[U];
 #pragma unroll
-      for (int u = 0; u < 4; u++) q[u] = __ldcs(p + i + u * blockDim.x);
+      for (int u = 0; u < U; u++) q[u] = __ldcs(p + i + u * blockDim.x);
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < U; u++) {
         const K* qk = reinterpret_cast<const K*>(&q[u]);
         atomicAdd(s_h + fine_of<H>(qk[0], hp, s), 1u);
         atomicAdd(s_h + fine_of<H>(qk[1], hp, s), 1u);
