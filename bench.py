@@ -203,6 +203,12 @@ def cpu_sample(log2: int, k: int, lf: float, workers: int):
 # --------------------------------------------------------------------------- reference arm
 
 
+def workload_name(args, kb: int = 32) -> str:
+    """The workload both arms report (BASELINE configs[4], one point of the sweep)."""
+    return (f"C5 weak scaling: 2^{args.log2_keys} uint{kb} keys + 2^{args.log2_keys} queries per GPU, "
+            + (f"keys from {{1..2^{args.k}}}" if kb == 32 else "full 64-bit SplitMix64 words") + f", C={args.load_factor}")
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -222,8 +228,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"C5 weak scaling sample: 2^{log2} keys+queries on host", "k": args.k,
-                   "load_factor": args.load_factor},
+        "config": {"workload": workload_name(args), "keys_per_gpu": 1 << args.log2_keys,
+                   "queries_per_gpu": 1 << args.log2_keys,
+                   "sample": f"each step times 2^{log2} keys + 2^{log2} queries of the same streams on the host"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -426,9 +433,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": f"u{kb}", "data": "synthetic",
-        "config": {"workload": (f"C5 weak scaling: 2^{args.log2_keys} uint{kb} keys + 2^{args.log2_keys} queries per "
-                                f"GPU, " + (f"keys from {{1..2^{args.k}}}" if kb == 32 else "full 64-bit SplitMix64 words")
-                                + f", C={args.load_factor}"),
+        "config": {"workload": workload_name(args, kb),
                    "keys_per_gpu": n, "queries_per_gpu": q, "hash_range_per_gpu": v,
                    "l2": "inputs (1 GiB per array) larger than the 126 MB L2",
                    "parallelism": "single-shard" if not use_dist else f"partitioned over {world} GPU(s) ({'fused peer-memory exchange' if args.transport == 'p2p' else 'NCCL alltoallv'})",
