@@ -133,53 +133,6 @@ __device__ uint32_t block_exscan(uint32_t* a, uint32_t n) {
   return total;
 }
 
-// Exclusive scan of nvals packed uint16 counters (two per word) in smem, in
-// place; totals stay < 65536.  Warp w owns a contiguous segment of words and
-// walks it in 32-word rows (lane = word within row: no bank conflicts).
-__device__ void block_exscan_u16(uint32_t* w16, uint32_t nvals) {
-  __shared__ uint32_t s_w[32];
-  const uint32_t nwords = (nvals + 1) / 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint32_t seg = ((nwords + nw - 1) / nw + 31) & ~31u;
-  const uint32_t w0 = warp * seg, w1 = min(w0 + seg, nwords);
-  uint32_t part = 0;
-  for (uint32_t i = w0 + lane; i < w1; i += 32) {
-    const uint32_t x = w16[i];
-    part += (x & 0xFFFFu) + (x >> 16);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  if (lane == 0) s_w[warp] = part;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t x = lane < nw ? s_w[lane] : 0u;
-    uint32_t inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    if (lane < nw) s_w[lane] = inc - x;  // exclusive warp bases
-  }
-  __syncthreads();
-  uint32_t carry = s_w[warp];
-  for (uint32_t r = w0; r < w1; r += 32) {
-    const uint32_t i = r + lane;
-    const uint32_t x = i < w1 ? w16[i] : 0u;
-    const uint32_t sx = (x & 0xFFFFu) + (x >> 16);
-    uint32_t inc = sx;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const uint32_t pre = carry + inc - sx;
-    if (i < w1) w16[i] = (pre & 0xFFFFu) | ((pre + (x & 0xFFFFu)) << 16);
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
-  __syncthreads();
-}
-
 // Exclusive scan of n uint32 in smem (in place), warp-row layout (no bank
 // conflicts); `base` is added to every output.  Returns the total.
 __device__ uint32_t block_exscan_rows(uint32_t* a, uint32_t n, uint32_t base) {
@@ -222,42 +175,6 @@ __device__ uint32_t block_exscan_rows(uint32_t* a, uint32_t n, uint32_t base) {
   }
   __syncthreads();
   return total;
-}
-
-// Inclusive max-scan of n (<= 32 * blockDim) uint32 in smem, in place.
-__device__ void block_maxscan(uint32_t* a, uint32_t n) {
-  __shared__ uint32_t s_w[32];
-  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, n);
-  uint32_t mx = 0;
-  for (uint32_t i = lo; i < hi; i++) mx = max(mx, a[i]);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t inc = mx;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc = max(inc, y);
-  }
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < nw ? s_w[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w = max(w, y);
-    }
-    if (lane < nw) s_w[lane] = w;
-  }
-  __syncthreads();
-  uint32_t run = warp ? s_w[warp - 1] : 0u;
-  const uint32_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane > 0) run = max(run, prev);
-  for (uint32_t i = lo; i < hi; i++) {
-    run = max(run, a[i]);
-    a[i] = run;
-  }
-  __syncthreads();
 }
 
 __device__ __forceinline__ uint32_t get16(const uint32_t* p, uint32_t k) { return (p[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu; }
@@ -548,14 +465,10 @@ __device__ __forceinline__ void store_runs(const PartSmem<K>& s, uint32_t nb, K*
       const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
       const uint32_t body = (cnt - h) & ~(kPadMod - 1);
       for (uint32_t i = 0; i < h; i++) out[g + i] = s.staged[p + i];
-#ifdef HG_NO_TMA_STORE
-      for (uint32_t i = h; i < h + body; i++) out[g + i] = s.staged[p + i];
-#else
       if (body) {
         tma_store_1d(out + g + h, s.staged + p + h, body * (uint32_t)sizeof(K));
         tma_store_commit();
       }
-#endif
       for (uint32_t i = h + body; i < cnt; i++) out[g + i] = s.staged[p + i];
     }
   }
