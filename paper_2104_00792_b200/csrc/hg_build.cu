@@ -346,9 +346,13 @@ int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const uint32_t*
 size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits) {
   size_t kb = key_bits / 8;
   size_t b = align_up(4 * (v + 1), 256) + align_up(kb * q, 256) + align_up(4 * q, 256) + build_ws_bytes(q, v, key_bits) + 1024;
-  // the binned layout depends on the table size; size for the worst case (table of v keys)
-  BinLayout L;
-  if (use_binned(v, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true));
+  // The binned layout depends on the table's keys per bucket (more keys per
+  // bucket -> smaller fine bins -> more of them -> more workspace), which this
+  // query does not know: size for every table density the binned path accepts.
+  for (int lg = 0; lg <= 16; lg++) {
+    BinLayout L;
+    if (use_binned(v << lg, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true));
+  }
   return b;
 }
 

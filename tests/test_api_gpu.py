@@ -319,3 +319,24 @@ def test_cuda_tensor_inputs_stay_on_device():
     assert r.multiplicities_device.is_cuda and r.matched_positions == keys.numel()
     h = hg.hash_array(MURMUR, keys, 1000)
     assert h.is_cuda and h.dtype == torch.int64
+
+
+@pytest.mark.parametrize("lf", [1.0, 2.0, 4.0, 8.0])
+def test_query_takes_binned_path_at_every_load_factor(lf):
+    """The query workspace is sized for any table density, so denser tables
+    (C > 1, BASELINE's C5 sweep) still run the binned query -- not the direct
+    Alg. 1 fallback -- and give the oracle's answers."""
+    from paper_2104_00792_b200 import _lib
+
+    rng = np.random.default_rng(int(lf * 10))
+    n = 1 << 20
+    keys = rng.integers(1, 1 << 21, size=n, dtype=np.uint64).astype(np.uint32)
+    queries = rng.integers(1, 1 << 21, size=n, dtype=np.uint64).astype(np.uint32)
+    table = hg.build(keys, lf)
+    _lib.timing_enable(True)
+    _lib.timing_collect()
+    res = hg.intersect(table, queries)
+    names = {name for name, _ in _lib.timing_collect()}
+    _lib.timing_enable(False)
+    assert "hg_local_probe" in names and "hg_place_pos" not in names, names
+    assert np.array_equal(res.multiplicities, O.count_occurrences(keys, queries))
