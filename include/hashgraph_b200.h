@@ -92,6 +92,13 @@ HG_API size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits);
 HG_API int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries,
              uint64_t q, int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult,
              uint64_t* agg, void* workspace, size_t workspace_bytes, void* stream);
+/* hg_query plus a split point for intersect_timed (query.py:193-202): split_event
+ * (a cudaEvent_t created by the caller) is recorded on the stream once the
+ * query-side table (the binned grouping of the queries, or the direct query
+ * CSR) is complete, before the intersection kernels. */
+HG_API int hg_query_timed(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries,
+                   uint64_t q, int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult,
+                   uint64_t* agg, void* workspace, size_t workspace_bytes, void* split_event, void* stream);
 
 /* Partitioned build, Phase 1 -- replaces the bin histogram of
  * multishard.build_sharded.worker (multishard.py:371-377) and

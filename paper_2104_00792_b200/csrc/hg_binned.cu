@@ -1597,11 +1597,13 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
 
 template <typename H>
 static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyOf<H>* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
+                 cudaEvent_t split) {
   using K = KeyOf<H>;
   PartOut po{};
   int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
   if (rc) return rc;
+  if (split) HG_CHECK_CUDA(cudaEventRecord(split, st));  // query-side grouping done (intersect_timed's split)
   uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
@@ -1656,9 +1658,10 @@ int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, co
 
 template <typename K>
 int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st) {
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
+                 cudaEvent_t split) {
   return with_hasher<K>(hp, [&](auto h) {
-    return query_impl<decltype(h)>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st);
+    return query_impl<decltype(h)>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st, split);
   });
 }
 
@@ -1667,8 +1670,10 @@ template int binned_build<uint32_t>(const uint32_t*, uint64_t, const HashParams&
 template int binned_build<uint64_t>(const uint64_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
                                     uint32_t*, uint64_t*, Workspace&, cudaStream_t);
 template int binned_query<uint32_t>(const uint32_t*, const uint32_t*, const uint32_t*, uint64_t, const HashParams&,
-                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t);
+                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t,
+                                    cudaEvent_t);
 template int binned_query<uint64_t>(const uint32_t*, const uint64_t*, const uint64_t*, uint64_t, const HashParams&,
-                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t);
+                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t,
+                                    cudaEvent_t);
 
 }  // namespace hg

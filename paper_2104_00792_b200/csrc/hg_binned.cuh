@@ -26,6 +26,7 @@ int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, co
                  K* edges, Workspace& ws, cudaStream_t st);
 template <typename K>
 int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st);
+                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
+                 cudaEvent_t split = nullptr);
 
 }  // namespace hg

@@ -356,9 +356,9 @@ size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits) {
   return b;
 }
 
-int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries, uint64_t q,
-             int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* workspace,
-             size_t workspace_bytes, void* stream) {
+static int query_entry(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries, uint64_t q,
+                       int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg,
+                       void* workspace, size_t workspace_bytes, void* stream, cudaEvent_t split) {
   int rc = check_common(q, key_bits, kind, v);
   if (rc) return rc;
   Workspace ws{(char*)workspace, workspace_bytes, 0};
@@ -369,9 +369,9 @@ int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const
     if (agg) HG_CHECK_CUDA(cudaMemsetAsync(agg, 0, 24, s));
     if (key_bits == 32)
       return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)queries, q, hp, v, L, mult,
-                                    agg, ws, s);
+                                    agg, ws, s, split);
     return binned_query<uint64_t>(offsets_a, (const uint64_t*)edges_a, (const uint64_t*)queries, q, hp, v, L, mult,
-                                  agg, ws, s);
+                                  agg, ws, s, split);
   }
   size_t kb = key_bits / 8;
   uint32_t* qoff = ws.take<uint32_t>(v + 1);
@@ -382,11 +382,27 @@ int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const
   if (key_bits == 32) {
     rc = build_impl<uint32_t>((const uint32_t*)queries, q, hp, v, qoff, (uint32_t*)qedges, qpos, rest, s);
     if (rc) return rc;
+    if (split) HG_CHECK_CUDA(cudaEventRecord(split, s));
     return intersect_impl<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)qedges, qpos, q, hp, mult, agg, s);
   }
   rc = build_impl<uint64_t>((const uint64_t*)queries, q, hp, v, qoff, (uint64_t*)qedges, qpos, rest, s);
   if (rc) return rc;
+  if (split) HG_CHECK_CUDA(cudaEventRecord(split, s));
   return intersect_impl<uint64_t>(offsets_a, (const uint64_t*)edges_a, (const uint64_t*)qedges, qpos, q, hp, mult, agg, s);
+}
+
+int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries, uint64_t q,
+             int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* workspace,
+             size_t workspace_bytes, void* stream) {
+  return query_entry(offsets_a, edges_a, n_a, queries, q, key_bits, kind, seed, v, mult, agg, workspace,
+                     workspace_bytes, stream, nullptr);
+}
+
+int hg_query_timed(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries, uint64_t q,
+                   int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* workspace,
+                   size_t workspace_bytes, void* split_event, void* stream) {
+  return query_entry(offsets_a, edges_a, n_a, queries, q, key_bits, kind, seed, v, mult, agg, workspace,
+                     workspace_bytes, stream, (cudaEvent_t)split_event);
 }
 
 }  // extern "C"

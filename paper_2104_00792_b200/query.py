@@ -167,7 +167,12 @@ def intersect(table, queries, worker_count: int = 1) -> QueryResult:
 
 
 def intersect_timed(table, queries, worker_count: int = 1):
-    """intersect() plus the build-vs-intersect split, in device nanoseconds (query.py:193-202)."""
+    """intersect() plus the build-vs-intersect split, in device nanoseconds (query.py:193-202).
+
+    Runs the same fused query as intersect(); the library records a split
+    event once the query-side table (the binned grouping of the queries) is
+    complete, so table_build_ns covers that and intersect_ns the probe and the
+    return to query order."""
     if worker_count < 1:
         raise ConfigError(f"worker count must be >= 1, got {worker_count}")
     t = D.require_cuda()
@@ -175,18 +180,19 @@ def intersect_timed(table, queries, worker_count: int = 1):
     if ta.hash_range > 1 << 32:
         raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
     qd = D.to_device_keys(queries, ta.key_bits)
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
-    ev[0].record()
-    q_off, q_edges, q_pos = build_device(qd, ta.hash_range, ta.family, ta.key_bits, want_positions=True)
-    ev[1].record()
     nb = qd.numel()
     mult = t.zeros(nb, dtype=t.int32, device=qd.device)
     agg = t.zeros(3, dtype=t.int64, device=qd.device)
     kind, seed = family_code(ta.family)
-    _lib.call("hg_intersect", D.ptr(ta.offset_device), D.ptr(ta.keys_device), D.ptr(q_off), D.ptr(q_edges),
-              D.ptr(q_pos), nb, ta.key_bits, kind, seed, ta.hash_range, D.ptr(mult), D.ptr(agg), D.stream_ptr())
+    ws = D.workspace(_lib.load().hg_query_workspace_size(nb, ta.hash_range, ta.key_bits))
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[1].record()  # creates the split event; the library re-records it at the split point
+    ev[0].record()
+    _lib.call("hg_query_timed", D.ptr(ta.offset_device), D.ptr(ta.keys_device), ta.num_keys, D.ptr(qd), nb,
+              ta.key_bits, kind, seed, ta.hash_range, D.ptr(mult), D.ptr(agg), D.ptr(ws), ws.numel(),
+              ev[1].cuda_event, D.stream_ptr())
     ev[2].record()
     ev[2].synchronize()
-    build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
-    inter_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
+    build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6) if nb else 0
+    inter_ns = int(ev[1].elapsed_time(ev[2]) * 1e6) if nb else 0
     return QueryResult(mult, agg, ta.hash_range), QueryStageTimes(build_ns, inter_ns)
