@@ -388,22 +388,39 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
     if (k & 1) rk[k >> 1] |= r << 16; else rk[k >> 1] = r;
   }
   __syncthreads();
-  uint32_t d = 0;
-  if (threadIdx.x < nb) {
-    uint32_t run = 0;
+  // Per-bin prefix over warps and the scan over bins, by the warps that own
+  // bins only (thread b = bin b), synchronised with a named barrier among
+  // them: the rest of the CTA waits at one barrier instead of four.
+  __shared__ uint32_t s_bw[kMaxBins / 32];
+  const uint32_t nbw = (nb + 31) / 32;  // warps that own bins (CTA-uniform)
+  if ((uint32_t)warp < nbw) {
+    const uint32_t b = threadIdx.x;
+    uint32_t run = 0, d = 0;
+    if (b < nb) {
 #pragma unroll
-    for (int w = 0; w < kW; w++) {
-      const uint32_t c = s.wcnt[w][threadIdx.x];
-      s.wcnt[w][threadIdx.x] = run;
-      run += c;
+      for (int w = 0; w < kW; w++) {
+        const uint32_t c = s.wcnt[w][b];
+        s.wcnt[w][b] = run;
+        run += c;
+      }
+      if (claims && run) d = atomicAdd(claims + b, run);
     }
-    s.toff[threadIdx.x] = run;
-    if (claims && run) d = atomicAdd(claims + threadIdx.x, run);
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_bw[warp] = inc;
+    named_barrier_sync(1, nbw * 32);
+    uint32_t base = 0;
+    for (int w = 0; w < warp; w++) base += s_bw[w];
+    if (b < nb) {
+      s.toff[b] = base + inc - run;
+      if (b == nb - 1) s.toff[nb] = base + inc;
+      if (claims) s.dst[b] = d;
+    }
   }
-  __syncthreads();
-  const uint32_t total = block_exscan(s.toff, nb);
-  if (threadIdx.x == 0) s.toff[nb] = total;
-  if (claims && threadIdx.x < nb) s.dst[threadIdx.x] = d;
   __syncthreads();
 }
 

@@ -256,6 +256,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // --------------------------------------------------------------------------- misc
 
+// bar.sync on a named barrier shared by `count` threads (a multiple of 32)
+__device__ __forceinline__ void named_barrier_sync(int id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
