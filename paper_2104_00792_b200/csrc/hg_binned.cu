@@ -591,6 +591,7 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
   // leaves (bin, first element, size) in smem: no global latency at the top
   // of a tile
   __shared__ uint32_t s_loc[3];
+  __shared__ uint32_t s_cur[3];  // the current tile's (bin, first, size), re-read after ranking: fewer live registers
   auto locate_issue = [&](uint32_t t) {
     uint32_t a = 0, z = nb1;  // level-1 bin c: tp[c] <= t < tp[c+1]
     while (z - a > 1) {
@@ -611,6 +612,11 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
   __syncthreads();  // s_loc of the first tile (later ones are ordered by the tile loop's barriers)
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint32_t c = s_loc[0], t0 = s_loc[1], m = s_loc[2];
+    if (!kQuery && threadIdx.x == 0) {  // build: re-read after ranking (measured: fewer spills); query: registers
+      s_cur[0] = c;
+      s_cur[1] = t0;
+      s_cur[2] = m;
+    }
     mbar_wait(&s.bar, parity);
     parity ^= 1;
     const uint32_t sh = t0 & (VPL - 1);
@@ -632,13 +638,13 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     __syncthreads();  // raw and s_loc consumed by every thread
     if (threadIdx.x == 0 && t + gridDim.x < ntiles) locate_issue(t + gridDim.x);
     uint32_t rk[KPT / 2];
-    rank_tile<K, KPT, false>(s, bp, rk, m, kSub, fine_cursor + c * kSub);
+    rank_tile<K, KPT, false>(s, bp, rk, kQuery ? m : s_cur[2], kSub, fine_cursor + (kQuery ? c : s_cur[0]) * kSub);
     if (kQuery) {
       if (threadIdx.x < kSub) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
     }
     pad_bases(s.pt, s.wcnt, s.toff, s.dst, kSub);
-    place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
+    place_tile<K, KPT, false>(s, kv, bp, rk, kQuery ? m : s_cur[2], kQuery ? pmap + t0 : nullptr);
     store_runs<K>(s, kSub, out);
   }
   if (threadIdx.x < kSub) tma_store_wait_all();
