@@ -367,8 +367,9 @@ __device__ __forceinline__ uint32_t pad_start(uint32_t toff, uint32_t b, uint32_
 
 // Rank a register tile by bin: one atomic on the warp's private bin counter
 // per key (rank kept in registers), then a per-bin prefix over warps.  On
-// return s.wcnt[w][b] is warp w's offset inside bin b's run and s.toff the
-// tile offsets (s.toff[nb] = tile size).
+// return s.toff holds the tile offsets (s.toff[nb] = tile size), s.pt each
+// run's padded staged start (congruent to s.dst[b] mod 4) and s.wcnt[w][b]
+// warp w's first staged slot in bin b.
 //
 // claims != nullptr (level 2): each bin's space is claimed (atomicAdd on
 // claims[b]) as soon as the bin's total is known, and the answer lands in
@@ -416,24 +417,17 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
     uint32_t base = 0;
     for (int w = 0; w < warp; w++) base += s_bw[w];
     if (b < nb) {
-      s.toff[b] = base + inc - run;
+      const uint32_t toff_b = base + inc - run;
+      s.toff[b] = toff_b;
       if (b == nb - 1) s.toff[nb] = base + inc;
       if (claims) s.dst[b] = d;
-    }
-  }
-  __syncthreads();
-}
-
-// Given s.dst, compute each bin's padded staged start and turn the warp
-// offsets into absolute staged slots.
-__device__ __forceinline__ void pad_bases(uint32_t* pt, uint32_t (*wcnt)[kMaxBins], const uint32_t* toff,
-                                          const uint32_t* dst, uint32_t nb) {
-  if (threadIdx.x < nb) {
-    const uint32_t b = threadIdx.x;
-    const uint32_t p = pad_start(toff[b], b, dst[b]);
-    pt[b] = p;
+      else d = s.dst[b];
+      // padded staged start of the run; the warps' offsets become absolute slots
+      const uint32_t p = pad_start(toff_b, b, d);
+      s.pt[b] = p;
 #pragma unroll
-    for (int w = 0; w < kW; w++) wcnt[w][b] += p;
+      for (int w = 0; w < kW; w++) s.wcnt[w][b] += p;
+    }
   }
   __syncthreads();
 }
@@ -552,7 +546,6 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
     uint32_t rk[KPT / 2];
     if (vec) rank_tile<K, KPT, true>(s, bp, rk, m, nb1);
     else rank_tile<K, KPT, false>(s, bp, rk, m, nb1);
-    pad_bases(s.pt, s.wcnt, s.toff, s.dst, nb1);
     if (vec) place_tile<K, KPT, true>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     else place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     if (kQuery)
@@ -643,7 +636,6 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
       if (threadIdx.x < kSub) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
       for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
     }
-    pad_bases(s.pt, s.wcnt, s.toff, s.dst, kSub);
     place_tile<K, KPT, false>(s, kv, bp, rk, kQuery ? m : s_cur[2], kQuery ? pmap + t0 : nullptr);
     store_runs<K>(s, kSub, out);
   }
