@@ -374,9 +374,18 @@ __device__ __forceinline__ uint32_t pad_start(uint32_t toff, uint32_t b, uint32_
 // claims != nullptr (level 2): each bin's space is claimed (atomicAdd on
 // claims[b]) as soon as the bin's total is known, and the answer lands in
 // s.dst[b] after the bin scan, so the atomic's latency overlaps the scan.
-template <typename K, int KPT, bool kFull>
+//
+// after_count() runs right after the counting barrier (every thread has
+// finished reading the tile's raw keys by then): the caller lands the next
+// tile there, with no barrier of its own.
+struct NoOp {
+  __device__ void operator()() const {}
+};
+
+template <typename K, int KPT, bool kFull, typename F = NoOp>
 __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[KPT / 4], uint32_t (&rk)[KPT / 2],
-                                          uint32_t m, uint32_t nb, uint32_t* __restrict__ claims = nullptr) {
+                                          uint32_t m, uint32_t nb, uint32_t* __restrict__ claims = nullptr,
+                                          F after_count = F()) {
   constexpr bool vec = kFull;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t b = lane; b < nb; b += 32) s.wcnt[warp][b] = 0;
@@ -389,6 +398,7 @@ __device__ __forceinline__ void rank_tile(PartSmem<K>& s, const uint32_t (&bp)[K
     if (k & 1) rk[k >> 1] |= r << 16; else rk[k >> 1] = r;
   }
   __syncthreads();
+  after_count();
   // Per-bin prefix over warps and the scan over bins, by the warps that own
   // bins only (thread b = bin b), synchronised with a named barrier among
   // them: the rest of the CTA waits at one barrier instead of four.
@@ -538,14 +548,15 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= (b & 0xFFu) << ((k & 3) * 8);
     }
-    if (threadIdx.x < nb1) tma_store_wait_read();  // previous tile's runs have left smem
-    fence_proxy_async();
-    __syncthreads();  // raw consumed, staged free
-    if (threadIdx.x == 0 && tma && t0 + 2 * TS::kTile <= hi)
-      tma_load_1d(s.raw, keys + t0 + TS::kTile, TS::kTile * sizeof(K), &s.bar);
+    if (threadIdx.x < nb1) tma_store_wait_read();  // previous tile's runs have left smem (before placement)
+    fence_proxy_async();                            // raw reads ordered before the next tile's TMA write
+    auto prefetch = [&] {
+      if (threadIdx.x == 0 && tma && t0 + 2 * TS::kTile <= hi)
+        tma_load_1d(s.raw, keys + t0 + TS::kTile, TS::kTile * sizeof(K), &s.bar);
+    };
     uint32_t rk[KPT / 2];
-    if (vec) rank_tile<K, KPT, true>(s, bp, rk, m, nb1);
-    else rank_tile<K, KPT, false>(s, bp, rk, m, nb1);
+    if (vec) rank_tile<K, KPT, true>(s, bp, rk, m, nb1, nullptr, prefetch);
+    else rank_tile<K, KPT, false>(s, bp, rk, m, nb1, nullptr, prefetch);
     if (vec) place_tile<K, KPT, true>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     else place_tile<K, KPT, false>(s, kv, bp, rk, m, kQuery ? pmap + t0 : nullptr);
     if (kQuery)
