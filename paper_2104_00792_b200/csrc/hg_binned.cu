@@ -959,6 +959,9 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
   }
   __syncthreads();
   if (f < nfine) fetch(f);
+  // tail keys written by threads 0..VPL-1 (only for the array's last bin) are
+  // visible after this barrier; later fetches are ordered by a bin's barriers
+  __syncthreads();
   uint32_t parity = 0;
   while (f < nfine) {
     const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
@@ -970,7 +973,6 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     const uint32_t fn = next_small(f + gridDim.x);
     mbar_wait(&s_bar, parity);
     parity ^= 1;
-    __syncthreads();  // the tail keys written by threads 0..VPL-1 are visible
     K kv[CPT * VPL];
     const uint4* raw4 = reinterpret_cast<const uint4*>(raw);
 #pragma unroll
