@@ -195,7 +195,7 @@ __global__ void k_intersect(const uint32_t* __restrict__ off_a, const K* __restr
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_b;
        j += (uint64_t)gridDim.x * blockDim.x) {
     K q = edges_b[j];
-    uint32_t h = bucket_of(q, hp);
+    const uint64_t h = hash_mod(q, hp);  // 64-bit: h + 1 == 2^32 when v == 2^32
     uint32_t lo = off_a[h], hi = off_a[h + 1];
     uint32_t c = 0;
     for (uint32_t t = lo; t < hi; t++) c += (edges_a[t] == q);
@@ -366,7 +366,6 @@ static int query_entry(const uint32_t* offsets_a, const void* edges_a, uint64_t 
   cudaStream_t s = (cudaStream_t)stream;
   BinLayout L;
   if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, true) <= workspace_bytes) {
-    if (agg) HG_CHECK_CUDA(cudaMemsetAsync(agg, 0, 24, s));
     if (key_bits == 32)
       return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)queries, q, hp, v, L, mult,
                                     agg, ws, s, split);

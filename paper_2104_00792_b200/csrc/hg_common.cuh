@@ -278,6 +278,18 @@ inline int num_sms() {
   return sms;
 }
 
+// opt-in dynamic shared memory per CTA (227 KB on sm_100)
+inline int max_dyn_smem() {
+  static int bytes = 0;
+  if (!bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&bytes, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (bytes <= 0) bytes = 232448;
+  }
+  return bytes;
+}
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Simple bump allocator over a caller-provided workspace.

@@ -484,6 +484,10 @@ static int reorg_count(const void* keys, uint64_t n, int key_bits, const HashPar
                        uint32_t* tile_counts, unsigned long long* totals, cudaStream_t s) {
   const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
   const size_t smem_c = 8 * (shards + 1) + 4 * shards;
+  if (key_bits == 32)
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_count<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+  else
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_count<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
   if (key_bits == 32) {
     HG_LAUNCH("hg_reorg_count", k_reorg_count<uint32_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
               (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
@@ -508,6 +512,11 @@ static int reorg_place(const void* keys, uint64_t n, int key_bits, const HashPar
   const auto* ro = (const unsigned long long*)row_offsets;
   const auto* dp_ = (const unsigned long long*)dest_ptrs;
   const auto* db = (const unsigned long long*)dest_base;
+  // up to 224 KB at 4096 shards (reorg_check bounds the shard count by the opt-in limit)
+  if (key_bits == 32)
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_place<uint32_t, kPeer>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+  else
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_place<uint64_t, kPeer>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
   if (key_bits == 32) {
     HG_LAUNCH("hg_reorg_place", (k_reorg_place<uint32_t, kPeer>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
               (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, (uint32_t*)grouped,
@@ -524,6 +533,10 @@ static int reorg_check(int key_bits, int kind, uint64_t hash_range, uint32_t sha
   int rc = check_hash(key_bits, kind, hash_range);
   if (rc) return rc;
   if (shards < 1 || shards > 4096) return set_error(HG_ERR_CONFIG, "shard count must be in [1, 4096], got %u", shards);
+  // k_reorg_place's peer variant stages 8 (P+1) + 16 P + 4 * warps * P bytes of shared memory
+  const size_t need = 8 * ((size_t)shards + 1) + 16 * (size_t)shards + 4 * (size_t)kReorgWarps * shards;
+  if (need > (size_t)max_dyn_smem())
+    return set_error(HG_ERR_CONFIG, "%u shards need %zu bytes of shared memory per CTA (limit %d)", shards, need, max_dyn_smem());
   if (bin_size < 1) return set_error(HG_ERR_CONFIG, "bin_size must be >= 1");
   if (n >= (1ull << 32)) return set_error(HG_ERR_CONFIG, "a shard holds fewer than 2^32 keys");
   return HG_OK;
@@ -695,6 +708,10 @@ int hg_route(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed
 int hg_return_peers(const uint32_t* vals, uint64_t n, const uint64_t* recv_bounds, const uint64_t* back_ptrs,
                     const uint64_t* back_base, uint32_t shards, void* stream) {
   if (shards < 1 || shards > 4096) return set_error(HG_ERR_CONFIG, "shard count must be in [1, 4096], got %u", shards);
+  // k_reorg_place's peer variant stages 8 (P+1) + 16 P + 4 * warps * P bytes of shared memory
+  const size_t need = 8 * ((size_t)shards + 1) + 16 * (size_t)shards + 4 * (size_t)kReorgWarps * shards;
+  if (need > (size_t)max_dyn_smem())
+    return set_error(HG_ERR_CONFIG, "%u shards need %zu bytes of shared memory per CTA (limit %d)", shards, need, max_dyn_smem());
   if (!n) return HG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   HG_LAUNCH("hg_return_peers", k_return_peers, grid_cap(n, 8), kT, 8 * (3 * (size_t)shards + 1), s, vals, n,

@@ -216,8 +216,14 @@ class PeerBuffers:
             import torch.distributed as dist
 
             t = D.torch()
+            # Capability is decided locally first (import + a local symmetric
+            # allocation, no collective), agreed by all_reduce(MIN), and only
+            # then does any rank enter the collective rendezvous: a rank that
+            # cannot use peer memory never leaves the others blocked in it.
             try:
-                self.get("probe", 1 << 10, t.int32)
+                import torch.distributed._symmetric_memory as symm_mem
+
+                symm_mem.empty(1 << 10, dtype=t.int32, device=D.device())
                 ok = 1
             except Exception as e:  # no symmetric-memory support: NCCL alltoallv instead
                 warnings.warn(f"peer-memory exchange unavailable ({e}); using NCCL all_to_all")
@@ -225,6 +231,8 @@ class PeerBuffers:
             flag = t.tensor([ok], dtype=t.int32, device=D.device())
             dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
             self._ok = bool(int(flag.item()))
+            if self._ok:
+                self.get("probe", 1 << 10, t.int32)  # collective: every rank agreed to enter
         return self._ok
 
     def get(self, name: str, n: int, dtype):

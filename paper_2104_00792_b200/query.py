@@ -154,6 +154,33 @@ def query_device(table: HashGraph, queries_dev):
     return mult, agg
 
 
+def _query_keys(table: HashGraph, queries):
+    """Queries on the device at the table's key width.
+
+    A 32-bit table refuses 64-bit queries that do not fit in 32 bits (a KEY8
+    file or 64-bit workload against an HGR1 table): the reference's silent
+    uint32 truncation (core.py:84-88) would report spurious matches for them.
+    Narrower queries against a 64-bit table are widened (lossless)."""
+    if table.key_bits == 32:
+        wide = None
+        if D.is_tensor(queries) and queries.element_size() == 8:
+            wide = queries
+        elif not D.is_tensor(queries):
+            arr = np.asarray(queries)
+            if arr.dtype.kind in "iu" and arr.dtype.itemsize == 8 and arr.size:
+                lo, hi = int(arr.min()), int(arr.max())
+                if lo < 0 or hi > 0xFFFFFFFF:
+                    raise ConfigError("64-bit query keys do not fit the table's 32-bit keys (build the table "
+                                      "with key_bits=64)")
+        if wide is not None and wide.numel():
+            t = D.torch()
+            w = wide.view(t.int64) if wide.dtype != t.int64 else wide
+            if bool(((w < 0) | (w > 0xFFFFFFFF)).any()):
+                raise ConfigError("64-bit query keys do not fit the table's 32-bit keys (build the table "
+                                  "with key_bits=64)")
+    return D.to_device_keys(queries, table.key_bits)
+
+
 def intersect(table, queries, worker_count: int = 1) -> QueryResult:
     """Count each query key's occurrences in the table (query.py:182-190)."""
     if worker_count < 1:
@@ -161,7 +188,7 @@ def intersect(table, queries, worker_count: int = 1) -> QueryResult:
     ta = as_device_table(table)
     if ta.hash_range > 1 << 32:
         raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
-    qd = D.to_device_keys(queries, ta.key_bits)
+    qd = _query_keys(ta, queries)
     mult, agg = query_device(ta, qd)
     return QueryResult(mult, agg, ta.hash_range)
 
@@ -179,7 +206,7 @@ def intersect_timed(table, queries, worker_count: int = 1):
     ta = as_device_table(table)
     if ta.hash_range > 1 << 32:
         raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
-    qd = D.to_device_keys(queries, ta.key_bits)
+    qd = _query_keys(ta, queries)
     nb = qd.numel()
     mult = t.zeros(nb, dtype=t.int32, device=qd.device)
     agg = t.zeros(3, dtype=t.int64, device=qd.device)
