@@ -38,6 +38,13 @@ METRIC = "HashGraph build+query keys/sec at 1/2/4/8 B200; achieved HBM & NVLink 
 UNIT = "keys/s"
 QUERY_SEED = 0x51
 
+# The oracle's answer for a bench workload, keyed by (log2 keys, k, load
+# factor, key bits): the timed step's aggregates must equal it (checked after
+# the timed region; tests/test_scale_parity_gpu.py recomputes it with oracle/).
+EXPECTED = {
+    (28, 28, 1.0, 32): {"matched": 169_672_492, "total": 268_422_361, "comparisons": 517_428_761},
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -146,6 +153,16 @@ def algorithmic_bytes(name: str, n: int, q: int, v: int, w: int = 4) -> float:
         "hg_unpart1": 4 * q + 2 * q + 4 * q,
     }
     return float(table.get(name, 0))
+
+
+def a_build(n: int, v: int, w: int = 4) -> float:
+    """A_build = 3 N w + 4 (V + 1)."""
+    return 3.0 * n * w + 4.0 * (v + 1)
+
+
+def a_query(n: int, q: int, v: int, w: int = 4) -> float:
+    """A_query = 4 Q w + 12 Q + N w + 12 (V + 1)."""
+    return 4.0 * q * w + 12.0 * q + n * w + 12.0 * (v + 1)
 
 
 def summarize_kernels(records, steps, n, q, v, peak, w=4):
@@ -350,11 +367,55 @@ def main():
     total_units = (n + q) * world * args.steps
     value = total_units / (elapsed_ms / 1e3)
 
+    # the timed step's answer against the oracle's (EXPECTED; N=1 single-shard)
+    check = None
+    if not use_dist:
+        exp = EXPECTED.get((args.log2_keys, args.k, float(args.load_factor), kb)) if kb == 32 else None
+        got = {"matched": res.matched_positions, "total": res.total_matches, "comparisons": res.comparisons}
+        check = {"step_aggregates": got, "expected": exp, "ok": (got == exp) if exp else None}
+        if exp and got != exp:
+            print(f"bench: timed step's aggregates {got} differ from the oracle's {exp}", file=sys.stderr)
+            sys.exit(3)
+
+    # build and query timed apart (graph replays, same inputs): the SURVEY
+    # 8(d3) fractions of the whole build, the whole query and the step
+    phases = None
+    if use_graph:
+        gb, gq = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gb):
+            tb = hg.build(keys, args.load_factor, key_bits=kb)
+        with torch.cuda.graph(gq):
+            hg.intersect(tb, queries)
+        gb.replay()
+        gq.replay()
+        reps = max(3, args.steps // 2)
+        ms = {}
+        for name, g in (("build", gb), ("query", gq)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ms[name] = a.elapsed_time(b) / reps
+        del gb, gq, tb
+        phases = {"build_ms": ms["build"], "query_ms": ms["query"], "replays": reps}
+
     peak, peak_kind = measured_peak()
     kernels, roof = summarize_kernels(records, args.steps, n, q, v, peak, kb // 8)
     if roof:
         roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback"
         roof["traffic"] = load_traffic(roof["kernel"])
+        w = kb // 8
+        ab, aq = a_build(n, v, w), a_query(n, q, v, w)
+        step_ms = elapsed_ms / args.steps
+        roof["step_frac"] = (ab + aq) / (step_ms / 1e3) / (peak * 1e9)
+        roof["algorithmic_bytes"] = {"build": ab, "query": aq, "formula": "SURVEY 8(d3): 3Nw+4(V+1); 4Qw+12Q+Nw+12(V+1)"}
+        if phases:
+            roof["build_frac"] = ab / (phases["build_ms"] / 1e3) / (peak * 1e9)
+            roof["query_frac"] = aq / (phases["query_ms"] / 1e3) / (peak * 1e9)
+            roof.update({"build_ms": phases["build_ms"], "query_ms": phases["query_ms"]})
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -415,6 +476,32 @@ def main():
                "ms_per_step": e2e_s / args.e2e_steps * 1e3,
                "pipeline": "2 steps in flight on 2 streams; host waits for and reads each result before reusing its buffer"}
 
+    # end to end as a caller of the reference API sees it: numpy keys and
+    # queries in, build + intersect, then the int64 multiplicities and the
+    # aggregates read back (pageable host memory, one step at a time)
+    e2e_ref = None
+    if not args.no_e2e and not use_dist and world == 1:
+        npk = keys.cpu().numpy().view(np.uint32 if kb == 32 else np.uint64)
+        npq = queries.cpu().numpy().view(np.uint32 if kb == 32 else np.uint64)
+
+        def ref_step():
+            t_ = hg.build(npk, args.load_factor, key_bits=kb)
+            r_ = hg.intersect(t_, npq)
+            m_ = r_.multiplicities
+            return int(m_[-1]) + r_.matched_positions + r_.total_matches + r_.comparisons
+
+        ref_step()
+        torch.cuda.synchronize()
+        reps = max(2, args.e2e_steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ref_step()
+        e2e_ref_s = (time.perf_counter() - t0) / reps
+        e2e_ref = {"value": (n + q) / e2e_ref_s, "unit": UNIT, "h2d_bytes_per_step": (kb // 8) * (n + q),
+                   "d2h_bytes_per_step": 8 * q + 24, "ms_per_step": e2e_ref_s * 1e3,
+                   "api": "hg.build(numpy keys); hg.intersect(table, numpy queries).multiplicities (int64) + "
+                          "matched_positions/total_matches/comparisons; pageable host memory, one step at a time"}
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -438,8 +525,8 @@ def main():
                    "l2": "inputs (1 GiB per array) larger than the 126 MB L2",
                    "parallelism": "single-shard" if not use_dist else f"partitioned over {world} GPU(s) ({'fused peer-memory exchange' if args.transport == 'p2p' else 'NCCL alltoallv'})",
                    "launch": "cuda_graph (one step captured, replayed per step)" if use_graph else "eager"},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-        "kernels": kernels,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_reference_api": e2e_ref, "gpu_launches": launches,
+        "clocks": clocks, "check": check, "kernels": kernels,
     }
     print(json.dumps(line), flush=True)
     if dist:
