@@ -40,6 +40,15 @@ def device():
     return torch().device("cuda", torch().cuda.current_device())
 
 
+def on(where):
+    """Context manager making `where` (a CUDA tensor, torch.device or index) the
+    current device, so allocations, `device()` and `stream_ptr()` follow it."""
+    t = torch()
+    if is_tensor(where):
+        where = where.device
+    return t.cuda.device(where)
+
+
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 

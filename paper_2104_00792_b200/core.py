@@ -134,12 +134,13 @@ def build_device(keys_dev, v: int, family, key_bits: int = 32, want_positions: b
     t = D.torch()
     n = keys_dev.numel()
     kind, seed = family_code(family)
-    offsets = t.empty(v + 1, dtype=t.int32, device=keys_dev.device)
-    edges = t.empty(n, dtype=keys_dev.dtype, device=keys_dev.device)
-    positions = t.empty(n, dtype=t.int32, device=keys_dev.device) if want_positions else None
-    ws = D.workspace(_lib.load().hg_build_workspace_size(n, v, key_bits))
-    _lib.call("hg_build", D.ptr(keys_dev), n, key_bits, kind, seed, v, D.ptr(offsets), D.ptr(edges),
-              D.ptr(positions), D.ptr(ws), ws.numel(), D.stream_ptr())
+    with D.on(keys_dev):  # the keys' device and its current stream
+        offsets = t.empty(v + 1, dtype=t.int32, device=keys_dev.device)
+        edges = t.empty(n, dtype=keys_dev.dtype, device=keys_dev.device)
+        positions = t.empty(n, dtype=t.int32, device=keys_dev.device) if want_positions else None
+        ws = D.workspace(_lib.load().hg_build_workspace_size(n, v, key_bits))
+        _lib.call("hg_build", D.ptr(keys_dev), n, key_bits, kind, seed, v, D.ptr(offsets), D.ptr(edges),
+                  D.ptr(positions), D.ptr(ws), ws.numel(), D.stream_ptr())
     return offsets, edges, positions
 
 

@@ -1197,6 +1197,18 @@ __device__ __forceinline__ uint32_t map_slot(K key) {
   return (uint32_t)(fmix64((uint64_t)key) & (kMapSlots - 1));
 }
 
+// Slot keys are written and read with atomics while the map is being built
+// (the state word publishes them; racecheck-clean), plainly after the
+// building barrier.
+__device__ __forceinline__ void key_store(uint32_t* p, uint32_t k) { atomicExch(p, k); }
+__device__ __forceinline__ void key_store(uint64_t* p, uint64_t k) {
+  atomicExch(reinterpret_cast<unsigned long long*>(p), (unsigned long long)k);
+}
+__device__ __forceinline__ uint32_t key_load(uint32_t* p) { return atomicOr(p, 0u); }
+__device__ __forceinline__ uint64_t key_load(uint64_t* p) {
+  return atomicOr(reinterpret_cast<unsigned long long*>(p), 0ull);
+}
+
 // Add `add` occurrences of `key` (per lane; a slot is claimed with CAS and
 // published once its key is written).
 template <typename K>
@@ -1205,14 +1217,15 @@ __device__ __forceinline__ void map_add_n(BigMap<K>& m, K key, uint32_t add) {
   for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
     uint32_t st = atomicCAS(&m.state[i], 0u, 1u);
     if (st == 0) {  // claimed an empty slot
-      m.key[i] = key;
+      key_store(&m.key[i], key);
       __threadfence_block();
       atomicExch(&m.state[i], 2u);
       atomicAdd(&m.cnt[i], add);
       return;
     }
     while (st == 1) st = atomicAdd(&m.state[i], 0u);  // another thread is publishing this slot
-    if (*reinterpret_cast<volatile const K*>(&m.key[i]) == key) {
+    __threadfence_block();
+    if (key_load(&m.key[i]) == key) {
       atomicAdd(&m.cnt[i], add);
       return;
     }

@@ -1,16 +1,20 @@
 """Partitioned build across P shards (mirrors multishard.py of the reference).
 
 This module is the single-process drop-in: P shard inputs in, P local tables
-out.  All P shards live on the current GPU ("virtual shards", the analogue of
-the reference's shard threads, multishard.py:414-419), so every phase is the
-same sm_100a kernel the multi-GPU path runs:
+out, all driven from the calling thread.  With one GPU per shard visible (or
+an explicit `devices=` list) shard d lives on GPU d; otherwise the P shards
+are "virtual shards" of the current GPU (the analogue of the reference's shard
+threads, multishard.py:414-419).  Every phase is the same sm_100a kernel:
 
-  Phase 1  hg_bin_histogram (per shard, accumulated) + hg_split_plan
+  Phase 1  hg_bin_histogram (per device, summed on shard 0's) + hg_split_plan
   Phase 2  hg_reorganize   (stable per-destination CSR, search-step counter)
-  Phase 3  device-to-device row gathers in ascending sender order
+  Phase 3  row copies into each owner's receive buffer, ascending sender order
+           (device-to-device over NVLink between GPUs; one concatenation on
+           one GPU)
   Phase 4  hg_build with the local range V_d = ceil(N_d / C)
 
-The one-process-per-GPU version over NCCL is `paper_2104_00792_b200.distributed`.
+The one-process-per-GPU version over NCCL / symmetric memory is
+`paper_2104_00792_b200.distributed`.
 """
 
 from __future__ import annotations
@@ -102,6 +106,7 @@ class PartitionPlan:
         return np.searchsorted(self.boundaries, hashes, side="right") - 1
 
     def splits_device(self):
+        """bin_splits as an int64 tensor on the current device."""
         return D.torch().from_numpy(np.array(self.bin_splits, dtype=np.int64)).to(D.device())
 
 
@@ -204,6 +209,11 @@ class ShardedHashGraph:
     @property
     def total_keys(self) -> int:
         return sum(self.received_counts)
+
+    @property
+    def devices(self) -> list:
+        """The CUDA device holding each shard's table."""
+        return [sh.keys_device.device for sh in self.shards]
 
 
 @dataclass
@@ -358,70 +368,248 @@ def exchange(fabric: ExchangeFabric, all_buffers) -> list:
     return received
 
 
-def build_sharded(per_shard_inputs, config: ShardConfig, key_bits: int = 32):
-    """The four-phase build on virtual shards of one GPU (multishard.py:336-471).
+# Phase 3 between shards of one device is one concatenation; the per-row copy
+# path that runs between GPUs can be forced on one GPU (tests).
+_EXCHANGE_BY_ROWS = False
+
+
+def shard_devices(shards: int, devices=None) -> list:
+    """The CUDA device of every shard.
+
+    `devices=None` places shard d on GPU d when the process sees exactly
+    `shards` GPUs (more than one), the analogue of the reference's one thread
+    per shard (multishard.py:414-419) on real hardware; otherwise every shard
+    is a virtual shard on the current GPU.  An explicit list (ints or
+    torch.device, one per shard, repeats allowed) overrides that."""
+    t = D.torch()
+    cur = t.cuda.current_device()
+    if devices is None:
+        n = t.cuda.device_count()
+        return list(range(shards)) if shards > 1 and n == shards else [cur] * shards
+    out = []
+    for d in devices:
+        idx = d.index if isinstance(d, t.device) else int(d)
+        if idx is None:
+            idx = cur
+        if not 0 <= idx < t.cuda.device_count():
+            raise ConfigError(f"device {d!r} is not a visible CUDA device")
+        out.append(idx)
+    if len(out) != shards:
+        raise ConfigError(f"got {len(out)} devices for {shards} shards")
+    return out
+
+
+def build_sharded(per_shard_inputs, config: ShardConfig, key_bits: int = 32, devices=None):
+    """The four-phase build (multishard.py:336-471), one shard per GPU or as
+    virtual shards of one GPU (see `shard_devices`).
+
+    All shards are driven from this host thread; every phase is enqueued on
+    the shards' devices (their current streams).
+
+    * Virtual shards (one device): the shard inputs are concatenated once and
+      Phases 1-3 are ONE histogram, one split and ONE stable reorganize over
+      the concatenation -- its row d is exactly the exchange's gather(d)
+      (senders ascending, each in input order), so the exchange is a view.
+    * One shard per GPU: per-device histograms summed on shard 0's device,
+      the plan copied to every device, a stable reorganize per sender, and
+      each sender's row copied straight into the owner's receive buffer
+      (device-to-device over NVLink/NVSwitch with peer access, ordered after
+      the sender's Phase 2 and before the owner's Phase 4 by stream events).
+
+    Then a local build per shard with V_d = ceil(N_d / C).  The only host
+    sync is the send-row matrix the receive buffers are sized from.  Like
+    the reference (whose clock starts after input coercion, multishard.py:
+    348, 414), `total_time_ns` starts once the inputs are on the devices.
 
     Returns (ShardedHashGraph, PhaseReport)."""
     p = config.shards
     if len(per_shard_inputs) != p:
         raise ConfigError(f"got {len(per_shard_inputs)} shard inputs for {p} shards")
     t = D.require_cuda()
-    wall0 = time.perf_counter_ns()
-    arrays = _inputs_to_device(per_shard_inputs, key_bits)
-    n = sum(a.numel() for a in arrays)
-    hr, bins_g, bin_size = config.resolve(n)
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(5)]
-    steps = t.zeros(1, dtype=t.int64, device=D.device())
+    devs = shard_devices(p, devices)
+    if len(set(devs)) == 1 and not _EXCHANGE_BY_ROWS:
+        return _build_sharded_one_device(per_shard_inputs, config, key_bits, devs[0])
+    return _build_sharded_devices(per_shard_inputs, config, key_bits, devs)
 
-    ev[0].record()
-    counts = bin_histogram_device(arrays, hr, bins_g, bin_size, config.family, key_bits)
-    splits = split_plan_device(counts, bins_g, n, p)
-    ev[1].record()
-    sends = []
-    for a in arrays:
-        rows, grouped, _ = reorganize_device(a, hr, bin_size, splits, p, config.family, key_bits, steps=steps)
-        sends.append((rows, grouped))
-    ev[2].record()
-    # one host sync: row sizes decide the receive buffers and the local ranges
-    rows_host = t.stack([r for r, _ in sends]).cpu().numpy() if sends else np.zeros((0, p + 1), np.int64)
-    fabric = ExchangeFabric(p)
-    for s, (rows, grouped) in enumerate(sends):
-        fabric.post(s, SendBuffers(None, None, key_bits=key_bits, _device=(rows, grouped, rows_host[s])))
-    ev3 = t.cuda.Event(enable_timing=True)
-    ev3.record()
-    received = [fabric.gather_device(d) for d in range(p)]
-    ev[3].record()
-    tables = []
-    for r in received:
-        v_d = hash_range_for(r.numel(), config.load_factor)
-        off, edges, _ = build_device(r, v_d, config.family, key_bits)
-        tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits, r.numel()))
-    ev[4].record()
-    ev[4].synchronize()
-    total_ns = time.perf_counter_ns() - wall0
-    plan = PartitionPlan(p, hr, bins_g, bin_size, splits.cpu().numpy())
-    received_counts = [int(r.numel()) for r in received]
-    assert fabric.keys_moved == n, "exchange conservation violated"
-    search_steps = int(steps.cpu().item())
 
-    def ns(a, b):
-        return int(a.elapsed_time(b) * 1e6)
-
-    phase_ns = [ns(ev[0], ev[1]), ns(ev[1], ev[2]), ns(ev3, ev[3]), ns(ev[3], ev[4])]
-    table = ShardedHashGraph(plan, tables, config.family, received_counts)
+def _report(config, n, hr, bins_g, phase_ns, search_steps, keys_moved, bytes_moved, received_counts, total_ns):
+    assert keys_moved == n, "exchange conservation violated"
     passes = {name: n for name in PASS_NAMES}
     phases = {
         "partition": PhaseStats(time_ns=phase_ns[0], keys_touched=2 * n),
         "preprocess": PhaseStats(time_ns=phase_ns[1], keys_touched=2 * n, search_steps=search_steps),
-        "all_to_all": PhaseStats(time_ns=phase_ns[2], keys_touched=n, bytes_exchanged=fabric.bytes_moved),
+        "all_to_all": PhaseStats(time_ns=phase_ns[2], keys_touched=n, bytes_exchanged=bytes_moved),
         "table_construction": PhaseStats(time_ns=phase_ns[3], keys_touched=3 * n),
     }
-    report = PhaseReport(
-        shards=p, total_keys=n, hash_range=hr, bins_g=bins_g, load_factor=config.load_factor,
+    return PhaseReport(
+        shards=config.shards, total_keys=n, hash_range=hr, bins_g=bins_g, load_factor=config.load_factor,
         family=config.family, phases=phases, passes=passes, search_steps=search_steps,
-        bytes_exchanged=fabric.bytes_moved, shard_received_counts=received_counts, total_time_ns=total_ns,
+        bytes_exchanged=bytes_moved, shard_received_counts=received_counts, total_time_ns=total_ns,
         build_throughput=(n / (total_ns / 1e9)) if (n and total_ns) else 0.0,
     )
+
+
+def _local_tables(received, config, key_bits):
+    tables = []
+    for r in received:
+        v_d = hash_range_for(r.numel(), config.load_factor)
+        off, edges, _ = build_device(r, v_d, config.family, key_bits)  # on r's device
+        tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits, r.numel()))
+    return tables
+
+
+def _concat_inputs(per_shard_inputs, key_bits):
+    """The shard inputs as one contiguous device array (one H2D for host inputs)."""
+    t = D.torch()
+    if all(D.is_cuda_tensor(k) for k in per_shard_inputs):
+        parts = _inputs_to_device(per_shard_inputs, key_bits)
+        sizes = [a.numel() for a in parts]
+        flat = t.cat(parts) if len(parts) > 1 else parts[0]
+        return flat, sizes
+    host = []
+    for k in per_shard_inputs:
+        if D.is_tensor(k):
+            k = D.to_numpy_keys(k, key_bits) if k.is_cuda else k.numpy().view(D.np_key_dtype(key_bits))
+        host.append(D.coerce_host_keys(k, key_bits))
+    sizes = [len(a) for a in host]
+    flat = np.concatenate(host) if len(host) > 1 else host[0]
+    return D.to_device_keys(flat, key_bits), sizes
+
+
+def _build_sharded_one_device(per_shard_inputs, config, key_bits, dev):
+    t = D.torch()
+    p = config.shards
+    with D.on(dev):
+        flat, sizes = _concat_inputs(per_shard_inputs, key_bits)
+        n = flat.numel()
+        hr, bins_g, bin_size = config.resolve(n)
+        wall0 = time.perf_counter_ns()
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+        steps = t.zeros(1, dtype=t.int64, device=D.device())
+        ev[0].record()
+        counts = bin_histogram_device([flat], hr, bins_g, bin_size, config.family, key_bits)
+        splits = split_plan_device(counts, bins_g, n, p)
+        ev[1].record()
+        rows, grouped, _ = reorganize_device(flat, hr, bin_size, splits, p, config.family, key_bits, steps=steps)
+        ev[2].record()
+        rows_host = rows.cpu().numpy()  # the one host sync: the local ranges
+        received = [grouped[int(rows_host[d]):int(rows_host[d + 1])] for d in range(p)]  # gather(d), as views
+        tables = _local_tables(received, config, key_bits)
+        ev[3].record()
+        ev[3].synchronize()
+        total_ns = time.perf_counter_ns() - wall0
+        splits_host = splits.cpu().numpy()
+        search_steps = int(steps.cpu().item())
+
+    def ns(a, b):
+        return int(a.elapsed_time(b) * 1e6)
+
+    received_counts = [int(r.numel()) for r in received]
+    plan = PartitionPlan(p, hr, bins_g, bin_size, splits_host)
+    table = ShardedHashGraph(plan, tables, config.family, received_counts)
+    # the exchange is the reorganize's row layout itself: no device time of its own
+    phase_ns = [ns(ev[0], ev[1]), ns(ev[1], ev[2]), 0, ns(ev[2], ev[3])]
+    report = _report(config, n, hr, bins_g, phase_ns, search_steps, n, (key_bits // 8) * n, received_counts,
+                     total_ns)
+    return table, report
+
+
+def _build_sharded_devices(per_shard_inputs, config, key_bits, devs):
+    t = D.torch()
+    p = config.shards
+    distinct = sorted(set(devs))
+    home = devs[0]
+    arrays = []
+    for d, k in zip(devs, per_shard_inputs):
+        with D.on(d):
+            arrays.append(_inputs_to_device([k], key_bits)[0])
+    n = sum(a.numel() for a in arrays)
+    hr, bins_g, bin_size = config.resolve(n)
+    for d in distinct:  # inputs resident before the clock starts (reference: after coercion)
+        t.cuda.synchronize(d)
+    wall0 = time.perf_counter_ns()
+
+    def events():
+        out = {}
+        for d in distinct:
+            with D.on(d):
+                out[d] = t.cuda.Event(enable_timing=True)
+        return out
+
+    ev = [events() for _ in range(5)]
+
+    def mark(k):
+        for d in distinct:
+            with D.on(d):
+                ev[k][d].record()
+
+    mark(0)
+    # Phase 1: one histogram per device, summed on the home device; the plan
+    # is computed there and copied to every device
+    counts = {}
+    for d, a in zip(devs, arrays):
+        with D.on(d):
+            counts[d] = bin_histogram_device([a], hr, bins_g, bin_size, config.family, key_bits, counts.get(d))
+    with D.on(home):
+        total = counts[home]
+        for d in distinct:
+            if d != home:
+                total = total + counts[d].to(home)
+        splits_home = split_plan_device(total, bins_g, n, p)
+    splits = {d: (splits_home if d == home else splits_home.to(d)) for d in distinct}
+    mark(1)
+    # Phase 2: stable per-destination rows on each sender's device
+    steps = {}
+    sends = []
+    for d, a in zip(devs, arrays):
+        with D.on(d):
+            if d not in steps:
+                steps[d] = t.zeros(1, dtype=t.int64, device=D.device())
+            sends.append(reorganize_device(a, hr, bin_size, splits[d], p, config.family, key_bits,
+                                           steps=steps[d])[:2])
+    mark(2)
+    # one host sync: row sizes decide the receive buffers
+    rows_host = np.stack([r.cpu().numpy() for r, _ in sends])
+    fabric = ExchangeFabric(p)
+    for s_, (rows, grouped) in enumerate(sends):
+        fabric.post(s_, SendBuffers(None, None, key_bits=key_bits, _device=(rows, grouped, rows_host[s_])))
+    ev3 = events()
+    for d in distinct:
+        with D.on(d):
+            ev3[d].record()
+    # Phase 3: owner j receives row j of every sender, ascending sender order
+    received = []
+    for j, dj in enumerate(devs):
+        with D.on(dj):
+            sizes = rows_host[:, j + 1] - rows_host[:, j]
+            recv = t.empty(int(sizes.sum()), dtype=D.storage_dtype(key_bits), device=D.device())
+            o = 0
+            for s_ in range(p):
+                m = int(sizes[s_])
+                if m:
+                    recv[o:o + m].copy_(fabric.posted[s_].row_device(j), non_blocking=True)
+                o += m
+            fabric.keys_moved += int(sizes.sum())
+            fabric.bytes_moved += (key_bits // 8) * int(sizes.sum())
+            received.append(recv)
+    mark(3)
+    # Phase 4: local build on each owner's device
+    tables = _local_tables(received, config, key_bits)
+    mark(4)
+    for d in distinct:
+        ev[4][d].synchronize()
+    total_ns = time.perf_counter_ns() - wall0
+    plan = PartitionPlan(p, hr, bins_g, bin_size, splits_home.cpu().numpy())
+    received_counts = [int(r.numel()) for r in received]
+    search_steps = sum(int(x.cpu().item()) for x in steps.values())
+
+    def ns(a, b):  # a phase's device time: the mean over the shards' devices (multishard.py:436-447)
+        return int(np.mean([a[d].elapsed_time(b[d]) for d in distinct]) * 1e6)
+
+    phase_ns = [ns(ev[0], ev[1]), ns(ev[1], ev[2]), ns(ev3, ev[3]), ns(ev[3], ev[4])]
+    table = ShardedHashGraph(plan, tables, config.family, received_counts)
+    report = _report(config, n, hr, bins_g, phase_ns, search_steps, fabric.keys_moved, fabric.bytes_moved,
+                     received_counts, total_ns)
     return table, report
 
 
@@ -437,32 +625,39 @@ def query_sharded_timed(table: ShardedHashGraph, queries, worker_count: int = 1)
 
 
 def _query_sharded(table: ShardedHashGraph, queries, worker_count: int, timed: bool):
+    """Queries are routed on shard 0's device with the table's plan (stable
+    rows + the input order), each row is answered on its shard's device and
+    the uint32 answers come back to be scattered into input order there."""
     if worker_count < 1:
         raise ConfigError(f"worker count must be >= 1, got {worker_count}")
     t = D.require_cuda()
     plan = table.plan
     p = plan.shards
     key_bits = table.shards[0].key_bits if table.shards else 32
-    (q,) = _inputs_to_device([queries], key_bits)
-    nq = q.numel()
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
-    ev[0].record()
-    rows, grouped, order = reorganize_device(q, plan.hash_range, plan.bin_size, plan.splits_device(), p, table.family,
-                                             key_bits, want_order=True)
-    rows_h = rows.cpu().numpy()
-    mult = t.zeros(nq, dtype=t.int32, device=D.device())
-    agg = t.zeros(3, dtype=t.int64, device=D.device())
-    hash_values = 0
-    ev[1].record()
-    for d, shard in enumerate(table.shards):
-        lo, hi = int(rows_h[d]), int(rows_h[d + 1])
-        hash_values += shard.hash_range
-        if hi == lo:
-            continue
-        m_d, a_d = query_device(shard, grouped[lo:hi])
-        _lib.call("hg_scatter_u32", D.ptr(m_d), D.ptr(order[lo:hi]), hi - lo, D.ptr(mult), D.stream_ptr())
-        agg += a_d
-    ev[2].record()
+    home = table.shards[0].keys_device.device if table.shards else D.device()
+    with D.on(home):
+        (q,) = _inputs_to_device([queries], key_bits)
+        nq = q.numel()
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        rows, grouped, order = reorganize_device(q, plan.hash_range, plan.bin_size, plan.splits_device(), p,
+                                                 table.family, key_bits, want_order=True)
+        rows_h = rows.cpu().numpy()
+        mult = t.zeros(nq, dtype=t.int32, device=D.device())
+        agg = t.zeros(3, dtype=t.int64, device=D.device())
+        hash_values = 0
+        ev[1].record()
+        for d, shard in enumerate(table.shards):
+            lo, hi = int(rows_h[d]), int(rows_h[d + 1])
+            hash_values += shard.hash_range
+            if hi == lo:
+                continue
+            m_d, a_d = query_device(shard, grouped[lo:hi])  # on the shard's device
+            if m_d.device != mult.device:
+                m_d, a_d = m_d.to(mult.device), a_d.to(mult.device)
+            _lib.call("hg_scatter_u32", D.ptr(m_d), D.ptr(order[lo:hi]), hi - lo, D.ptr(mult), D.stream_ptr())
+            agg += a_d
+        ev[2].record()
     result = QueryResult(mult, agg, hash_values)
     if not timed:
         return result, None

@@ -125,6 +125,11 @@ def intersect_tables(table, query_table, positions, worker_count: int = 1) -> Qu
     """Intersect corresponding buckets of a prebuilt query table (query.py:120-179)."""
     _check_pair(table, query_table, worker_count)
     ta, tb = as_device_table(table), as_device_table(query_table)
+    with D.on(ta.keys_device):
+        return _intersect_tables_device(ta, tb, positions)
+
+
+def _intersect_tables_device(ta, tb, positions):
     t = D.torch()
     if D.is_cuda_tensor(positions):
         pos = positions.to(t.int32)
@@ -145,12 +150,15 @@ def query_device(table: HashGraph, queries_dev):
     t = D.torch()
     q = queries_dev.numel()
     kind, seed = family_code(table.family)
-    mult = t.empty(q, dtype=t.int32, device=queries_dev.device)
-    agg = t.zeros(3, dtype=t.int64, device=queries_dev.device)
-    ws = D.workspace(_lib.load().hg_query_workspace_size(q, table.hash_range, table.key_bits))
-    _lib.call("hg_query", D.ptr(table.offset_device), D.ptr(table.keys_device), table.num_keys, D.ptr(queries_dev),
-              q, table.key_bits, kind, seed, table.hash_range, D.ptr(mult), D.ptr(agg), D.ptr(ws), ws.numel(),
-              D.stream_ptr())
+    with D.on(table.keys_device):  # the table's device and its current stream
+        if queries_dev.device != table.keys_device.device:
+            queries_dev = queries_dev.to(table.keys_device.device)
+        mult = t.empty(q, dtype=t.int32, device=queries_dev.device)
+        agg = t.zeros(3, dtype=t.int64, device=queries_dev.device)
+        ws = D.workspace(_lib.load().hg_query_workspace_size(q, table.hash_range, table.key_bits))
+        _lib.call("hg_query", D.ptr(table.offset_device), D.ptr(table.keys_device), table.num_keys,
+                  D.ptr(queries_dev), q, table.key_bits, kind, seed, table.hash_range, D.ptr(mult), D.ptr(agg),
+                  D.ptr(ws), ws.numel(), D.stream_ptr())
     return mult, agg
 
 
@@ -188,8 +196,9 @@ def intersect(table, queries, worker_count: int = 1) -> QueryResult:
     ta = as_device_table(table)
     if ta.hash_range > 1 << 32:
         raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
-    qd = _query_keys(ta, queries)
-    mult, agg = query_device(ta, qd)
+    with D.on(ta.keys_device):
+        qd = _query_keys(ta, queries)
+        mult, agg = query_device(ta, qd)
     return QueryResult(mult, agg, ta.hash_range)
 
 
@@ -202,10 +211,16 @@ def intersect_timed(table, queries, worker_count: int = 1):
     return to query order."""
     if worker_count < 1:
         raise ConfigError(f"worker count must be >= 1, got {worker_count}")
-    t = D.require_cuda()
+    D.require_cuda()
     ta = as_device_table(table)
     if ta.hash_range > 1 << 32:
         raise ConfigError(f"hash range {ta.hash_range} exceeds the 2^32 intersection limit")
+    with D.on(ta.keys_device):
+        return _intersect_timed_device(ta, queries)
+
+
+def _intersect_timed_device(ta, queries):
+    t = D.torch()
     qd = _query_keys(ta, queries)
     nb = qd.numel()
     mult = t.zeros(nb, dtype=t.int32, device=qd.device)

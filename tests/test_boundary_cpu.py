@@ -5,6 +5,7 @@ product path refuses to run without a GPU (no host fallback)."""
 
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -77,3 +78,24 @@ def test_no_host_fallback_without_gpu():
         hg.build(np.arange(10, dtype=np.uint32))
     with pytest.raises(RuntimeError, match="CUDA"):
         hg.hash_array(hg.HashFamily(), np.arange(10, dtype=np.uint32), 7)
+
+
+def test_conformance_shim_maps_the_reference_names():
+    """tests/conformance/hashgraph binds every reference export and submodule
+    to this package (the reference suite runs through it on the GPU)."""
+    import importlib
+
+    sys.path.insert(0, os.path.join(ROOT, "tests", "conformance"))
+    try:
+        shim = importlib.import_module("hashgraph")
+        import paper_2104_00792_b200 as impl
+
+        assert shim.__file__.startswith(os.path.join(ROOT, "tests", "conformance"))
+        for name in impl.__all__:
+            assert getattr(shim, name) is getattr(impl, name)
+        for sub in ("cli", "core", "errors", "hashing", "multishard", "query", "workload"):
+            assert importlib.import_module(f"hashgraph.{sub}") is importlib.import_module(f"paper_2104_00792_b200.{sub}")
+    finally:
+        sys.path.remove(os.path.join(ROOT, "tests", "conformance"))
+        for k in [k for k in sys.modules if k == "hashgraph" or k.startswith("hashgraph.")]:
+            del sys.modules[k]
