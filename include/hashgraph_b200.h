@@ -89,8 +89,11 @@ HG_API int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const ui
  * table's v (build_query_table, query.py:84-95) and intersects.  mult is
  * uint32[q] in query order; agg (nullable, uint64[3]) is ACCUMULATED like
  * hg_intersect's (caller zeroes), whichever kernels the query runs, so several
- * shard queries can sum into one buffer. */
-HG_API size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits);
+ * shard queries can sum into one buffer.  The workspace depends on the table's
+ * key count n_table (its keys per bucket set the bin size; fine bins too large
+ * for shared memory -- high-duplicate or skewed tables -- are answered from a
+ * key -> count hash table of up to 2 * n_table slots). */
+HG_API size_t hg_query_workspace_size(uint64_t q, uint64_t v, uint64_t n_table, int key_bits);
 HG_API int hg_query(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const void* queries,
              uint64_t q, int key_bits, int kind, uint32_t seed, uint64_t v, uint32_t* mult,
              uint64_t* agg, void* workspace, size_t workspace_bytes, void* stream);

@@ -32,6 +32,7 @@ __all__ = [
     "hash_range_for",
     "coerce_keys",
     "build_csr",
+    "default_workers",
     "canonical",
     "intersect_csr",
     "query",

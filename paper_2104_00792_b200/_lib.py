@@ -37,7 +37,7 @@ SIGNATURES = {
                           _c_size, _c_ptr]),
     "hg_intersect": (_c_int, [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64,
                               _c_ptr, _c_ptr, _c_ptr]),
-    "hg_query_workspace_size": (_c_size, [_c_u64, _c_u64, _c_int]),
+    "hg_query_workspace_size": (_c_size, [_c_u64, _c_u64, _c_u64, _c_int]),
     "hg_query": (_c_int, [_c_ptr, _c_ptr, _c_u64, _c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_ptr, _c_ptr,
                           _c_ptr, _c_size, _c_ptr]),
     "hg_query_timed": (_c_int, [_c_ptr, _c_ptr, _c_u64, _c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_ptr, _c_ptr,

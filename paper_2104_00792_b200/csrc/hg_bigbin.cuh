@@ -1,0 +1,507 @@
+// hg_bigbin.cuh -- fine bins too large for shared memory (high-duplicate and
+// skewed inputs).  Part of hg_binned.cu (included there after its block
+// helpers); split out for size.
+//
+// A fine bin holds more than kCap keys only when many keys share few buckets:
+// all-identical keys, Zipf-like hot keys, or a hash range far below the key
+// count (acceptance c05/c06 sweep the duplicate rate, test_acceptance.py:
+// 160-196; the paper claims build throughput flat across it).
+// Such a bin must not serialise on one SM, so both sides work in chunks that
+// every CTA of the grid shares:
+//
+//   build   k_big_plan   chunk prefix over the oversized bins
+//           k_big_zero   zero their bucket counters (= the offsets slice)
+//           k_big_count  per chunk: smem counts, one global add per bucket
+//           k_big_scan   per bin: counts -> bucket starts (in offsets)
+//           k_big_place  per chunk: smem ranks, one global claim per bucket,
+//                        keys stored at claim + rank
+//           k_big_fix    per bin: claimed ends -> starts (shift by one)
+//   query   k_probe_plan per fine bin: shared-memory probe work items, or the
+//                        hash-table path when the table slice is oversized
+//           k_ht_clear   key -> count table (open addressing) for those bins
+//           k_ht_insert  their table keys, runs and warp peers aggregated
+//           k_ht_lookup  their queries: count from the table, comparisons
+//                        from the bucket degree (query.py:153-155)
+// (no include guard / namespace: textually included inside hg_binned.cu's namespace hg)
+
+// Block-wide exclusive scan of one value per thread (any blockDim <= 1024);
+// returns the exclusive prefix, `total` gets the block sum.  Three barriers.
+template <typename T>
+__device__ __forceinline__ T block_scan_excl(T x, T& total) {
+  __shared__ T s_ws[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  T inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < nw ? s_ws[lane] : T(0);
+    T wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    s_ws[lane] = wi - w;
+    if (lane == 31) s_ws[32] = wi;
+  }
+  __syncthreads();
+  const T r = s_ws[warp] + inc - x;
+  total = s_ws[32];
+  __syncthreads();
+  return r;
+}
+
+// Index j with pre[j] <= x < pre[j + 1] (pre ascending, pre[0] = 0, n entries + end).
+__device__ __forceinline__ uint32_t upper_index(const uint32_t* pre, uint32_t n, uint32_t x) {
+  uint32_t a = 0, z = n;
+  while (z - a > 1) {
+    const uint32_t m = (a + z) >> 1;
+    if (pre[m] <= x) a = m; else z = m;
+  }
+  return a;
+}
+
+// ============================================================================ build
+
+template <typename K>
+struct BigShape {
+  static constexpr int kThreads = 1024;
+  static constexpr int kKPT = sizeof(K) == 4 ? 16 : 8;  // keys per thread per chunk (registers)
+  static constexpr uint32_t kChunk = kKPT * kThreads;
+};
+
+// One CTA: big_cp[j] = chunks before oversized bin j; big_cp[nbig] = total.
+template <typename K>
+__global__ void __launch_bounds__(1024) k_big_plan(const uint32_t* __restrict__ fine_start,
+                                                   const uint32_t* __restrict__ big_list,
+                                                   const uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_cp) {
+  constexpr uint32_t CH = BigShape<K>::kChunk;
+  const uint32_t nbig = *big_count;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nbig; base += blockDim.x) {
+    const uint32_t j = base + threadIdx.x;
+    uint32_t c = 0;
+    if (j < nbig) {
+      const uint32_t f = big_list[j];
+      c = (fine_start[f + 1] - fine_start[f] + CH - 1) / CH;
+    }
+    uint32_t tot;
+    const uint32_t e = block_scan_excl<uint32_t>(c, tot);
+    if (j < nbig) big_cp[j] = carry + e;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) big_cp[nbig] = carry;
+}
+
+// Bucket counters of the oversized bins live in their offsets slice: zero it.
+__global__ void k_big_zero(const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count, int s,
+                           uint64_t v, uint32_t* __restrict__ offsets) {
+  const uint32_t nbig = *big_count;
+  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
+    const uint64_t first = (uint64_t)big_list[j] << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = 0;
+  }
+}
+
+// Locate chunk k: bin index j, fine bin f, key range [lo, hi).
+__device__ __forceinline__ void big_chunk(uint32_t k, uint32_t nbig, uint32_t CH, const uint32_t* __restrict__ big_cp,
+                                          const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ fine_start,
+                                          uint32_t* s_loc) {
+  if (threadIdx.x == 0) {
+    const uint32_t j = upper_index(big_cp, nbig, k);
+    const uint32_t f = big_list[j];
+    const uint32_t lo = fine_start[f] + (k - big_cp[j]) * CH;
+    s_loc[0] = f;
+    s_loc[1] = lo;
+    s_loc[2] = min(fine_start[f + 1], lo + CH);
+  }
+  __syncthreads();
+}
+
+// Per chunk: count keys per bucket in smem (lanes of a warp that hit the same
+// bucket share one atomic), then add the nonzero counters to the bin's global
+// counters.  `copy` (two partition levels: the grouped keys sit in `edges`)
+// also copies the chunk to `dst` so placement can overwrite edges.
+template <typename H>
+__global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__ src, KeyOf<H>* __restrict__ dst, int copy,
+                                                    const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
+                                                    const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_cp,
+                                                    HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets) {
+  using K = KeyOf<H>;
+  using BS = BigShape<K>;
+  extern __shared__ uint32_t cnt[];  // 2^s
+  __shared__ uint32_t s_loc[3];
+  const uint32_t nbig = *big_count;
+  const uint32_t nch = big_cp[nbig];
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
+    big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
+    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2];
+    const uint64_t first = (uint64_t)f << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = 0;
+    __syncthreads();
+    K kv[BS::kKPT];
+#pragma unroll
+    for (int u = 0; u < BS::kKPT; u++) {
+      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = j < hi ? src[j] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < BS::kKPT; u++) {
+      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = j < hi;
+      if (ok && copy) dst[j] = kv[u];
+      const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      if (ok && (peers & lt) == 0) atomicAdd(cnt + l, (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x)
+      if (cnt[l]) atomicAdd(offsets + first + l, cnt[l]);
+    __syncthreads();
+  }
+}
+
+// Per oversized bin: counts -> bucket starts (exclusive scan + the bin's first key).
+__global__ void __launch_bounds__(1024) k_big_scan(const uint32_t* __restrict__ fine_start,
+                                                   const uint32_t* __restrict__ big_list,
+                                                   const uint32_t* __restrict__ big_count, int s, uint64_t v,
+                                                   uint32_t* __restrict__ offsets) {
+  extern __shared__ uint32_t a[];  // 2^s
+  const uint32_t nbig = *big_count;
+  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
+    const uint32_t f = big_list[j];
+    const uint64_t first = (uint64_t)f << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) a[l] = offsets[first + l];
+    __syncthreads();
+    block_exscan_rows(a, nb, fine_start[f]);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = a[l];
+    __syncthreads();
+  }
+}
+
+// Per chunk: ranks from smem counters (warp peers share one atomic), one
+// global claim per nonzero bucket (the offsets slice is the cursor), then
+// every key stored at claim + rank.  Bucket order inside a bucket is free
+// (core.py:12-14).
+template <typename H>
+__global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__ src, const uint32_t* __restrict__ fine_start,
+                                                    const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count,
+                                                    const uint32_t* __restrict__ big_cp, HashParams hp, int s, uint64_t v,
+                                                    uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges) {
+  using K = KeyOf<H>;
+  using BS = BigShape<K>;
+  extern __shared__ uint32_t cnt[];  // 2^s
+  __shared__ uint32_t s_loc[3];
+  const uint32_t nbig = *big_count;
+  const uint32_t nch = big_cp[nbig];
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
+    big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
+    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2];
+    const uint64_t first = (uint64_t)f << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = 0;
+    __syncthreads();
+    K kv[BS::kKPT];
+    uint32_t lr[BS::kKPT];  // bucket << 16 | rank would overflow: bucket (<= 14 bits) and rank (< 2^17) packed below
+#pragma unroll
+    for (int u = 0; u < BS::kKPT; u++) {
+      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = j < hi ? src[j] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < BS::kKPT; u++) {
+      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = j < hi;
+      const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      const int leader = __ffs(peers) - 1;
+      uint32_t b0 = 0;
+      if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      // rank < kChunk <= 2^14 fits 15 bits; bucket < 2^s <= 2^14 fits 17 bits
+      lr[u] = ok ? (l << 15) | (b0 + __popc(peers & lt)) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) {
+      const uint32_t c = cnt[l];
+      if (c) cnt[l] = atomicAdd(offsets + first + l, c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < BS::kKPT; u++)
+      if (lr[u] != 0xFFFFFFFFu) edges[cnt[lr[u] >> 15] + (lr[u] & 0x7FFFu)] = kv[u];
+    __syncthreads();
+  }
+}
+
+// Per oversized bin: after placement every cursor holds its bucket's end, i.e.
+// the next bucket's start; shift by one bucket.
+__global__ void __launch_bounds__(1024) k_big_fix(const uint32_t* __restrict__ fine_start,
+                                                  const uint32_t* __restrict__ big_list,
+                                                  const uint32_t* __restrict__ big_count, int s, uint64_t v,
+                                                  uint32_t* __restrict__ offsets) {
+  extern __shared__ uint32_t a[];  // 2^s
+  const uint32_t nbig = *big_count;
+  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
+    const uint32_t f = big_list[j];
+    const uint64_t first = (uint64_t)f << s;
+    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) a[l] = offsets[first + l];
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = l ? a[l - 1] : fine_start[f];
+    __syncthreads();
+  }
+}
+
+// ============================================================================ query
+
+// plan words (uint64): items, big bins, big table keys, big queries, hash-table capacity, all-ones-key count
+enum : int { kPlanItems = 0, kPlanBig, kPlanBigT, kPlanBigQ, kPlanCap, kPlanOnes, kPlanWords };
+constexpr uint32_t kProbeChunk = 32768;  // queries per shared-memory probe work item
+
+// One CTA.  Fine bin f: tn table keys (t_off at the bin's bucket boundaries),
+// qn queries.  tn <= cap: ceil(qn / kProbeChunk) probe items (item_bin =
+// f | chunk << 15).  tn > cap and qn > 0: the hash-table path (big_bin,
+// big_t / big_q = prefixes of table keys / queries over those bins).
+// Each thread owns a contiguous run of bins; loads are issued before the scan.
+__global__ void __launch_bounds__(1024) k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t* __restrict__ q_start,
+                                                     uint32_t nfine, int s, uint64_t v, uint32_t cap,
+                                                     uint32_t* __restrict__ item_bin, uint32_t* __restrict__ big_bin,
+                                                     uint32_t* __restrict__ big_t, uint32_t* __restrict__ big_q,
+                                                     unsigned long long* __restrict__ plan) {
+  const uint32_t per = (nfine + blockDim.x - 1) / blockDim.x;
+  const uint32_t f0 = min(nfine, threadIdx.x * per), f1 = min(nfine, f0 + per);
+  auto tab = [&](uint32_t f) -> uint32_t { return t_off[min((uint64_t)f << s, v)]; };
+  // pass 1: per-thread sums (items, big bins, big table keys, big queries)
+  uint32_t si = 0, sb = 0, st = 0, sq = 0;
+  if (f0 < f1) {
+    uint32_t ta = tab(f0), qa = q_start[f0];
+    for (uint32_t f = f0; f < f1; f++) {
+      const uint32_t tb = tab(f + 1), qb = q_start[f + 1];
+      const uint32_t tn = tb - ta, qn = qb - qa;
+      if (qn) {
+        if (tn <= cap) si += (qn + kProbeChunk - 1) / kProbeChunk;
+        else {
+          sb++;
+          st += tn;
+          sq += qn;
+        }
+      }
+      ta = tb;
+      qa = qb;
+    }
+  }
+  uint32_t ti, tb_, tt, tq;
+  uint32_t ei = block_scan_excl<uint32_t>(si, ti);
+  uint32_t eb = block_scan_excl<uint32_t>(sb, tb_);
+  uint32_t et = block_scan_excl<uint32_t>(st, tt);
+  uint32_t eq = block_scan_excl<uint32_t>(sq, tq);
+  // pass 2: write (the loads hit L1/L2 now)
+  if (f0 < f1) {
+    uint32_t ta = tab(f0), qa = q_start[f0];
+    for (uint32_t f = f0; f < f1; f++) {
+      const uint32_t tb = tab(f + 1), qb = q_start[f + 1];
+      const uint32_t tn = tb - ta, qn = qb - qa;
+      if (qn) {
+        if (tn <= cap) {
+          const uint32_t k = (qn + kProbeChunk - 1) / kProbeChunk;
+          for (uint32_t c = 0; c < k; c++) item_bin[ei + c] = f | (c << 15);
+          ei += k;
+        } else {
+          big_bin[eb] = f;
+          big_t[eb] = et;
+          big_q[eb] = eq;
+          eb++;
+          et += tn;
+          eq += qn;
+        }
+      }
+      ta = tb;
+      qa = qb;
+    }
+  }
+  if (threadIdx.x == 0) {
+    big_t[tb_] = tt;
+    big_q[tb_] = tq;
+    plan[kPlanItems] = ti;
+    plan[kPlanBig] = tb_;
+    plan[kPlanBigT] = tt;
+    plan[kPlanBigQ] = tq;
+    unsigned long long c = 0;
+    if (tt) {
+      c = 1024;
+      while (c < 2ull * tt) c <<= 1;
+    }
+    plan[kPlanCap] = c;
+    plan[kPlanOnes] = 0;
+  }
+}
+
+template <typename K>
+__device__ __forceinline__ uint64_t ht_slot(K key) {
+  return fmix64((uint64_t)key * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull);
+}
+
+template <typename K>
+__global__ void k_ht_clear(const unsigned long long* __restrict__ plan, K* __restrict__ hk, uint32_t* __restrict__ hc) {
+  const uint64_t cap = plan[kPlanCap];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
+    hk[i] = ~K(0);
+    hc[i] = 0;
+  }
+}
+
+__device__ __forceinline__ uint32_t cas_key(uint32_t* p, uint32_t cmp, uint32_t val) { return atomicCAS(p, cmp, val); }
+__device__ __forceinline__ uint64_t cas_key(uint64_t* p, uint64_t cmp, uint64_t val) {
+  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp, (unsigned long long)val);
+}
+
+// Add `add` occurrences of `key`.  The all-ones key is the empty marker and is
+// counted in plan[kPlanOnes] instead.  Slots never return to empty, so a
+// stale read of an empty slot is settled by the CAS.
+template <typename K>
+__device__ __forceinline__ void ht_add(K* hk, uint32_t* hc, uint64_t cap, K key, uint32_t add, unsigned long long* ones) {
+  if (key == ~K(0)) {
+    atomicAdd(ones, (unsigned long long)add);
+    return;
+  }
+  uint64_t i = ht_slot(key) & (cap - 1);
+  for (;;) {
+    K cur = hk[i];
+    if (cur == ~K(0)) {
+      cur = cas_key(hk + i, ~K(0), key);
+      if (cur == ~K(0)) cur = key;
+    }
+    if (cur == key) {
+      atomicAdd(hc + i, add);
+      return;
+    }
+    i = (i + 1) & (cap - 1);
+  }
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t ht_count(const K* hk, const uint32_t* hc, uint64_t cap, K key, uint32_t ones) {
+  if (key == ~K(0)) return ones;
+  uint64_t i = ht_slot(key) & (cap - 1);
+  for (;;) {
+    const K cur = hk[i];
+    if (cur == key) return hc[i];
+    if (cur == ~K(0)) return 0;
+    i = (i + 1) & (cap - 1);
+  }
+}
+
+constexpr int kHtT = 512;
+constexpr int kHtKPT = 8;  // consecutive keys per thread: runs of equal keys are merged before inserting
+
+// Table keys of the hash-table bins.  Each CTA takes chunks of kHtT * kHtKPT
+// flattened keys; a bin holds more than `cap` >= one chunk of keys, so a chunk
+// spans at most two bins.
+template <typename H>
+__global__ void __launch_bounds__(kHtT) k_ht_insert(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t_edges,
+                                                    int s, uint64_t v, const uint32_t* __restrict__ big_bin,
+                                                    const uint32_t* __restrict__ big_t, unsigned long long* __restrict__ plan,
+                                                    KeyOf<H>* __restrict__ hk, uint32_t* __restrict__ hc) {
+  using K = KeyOf<H>;
+  constexpr uint32_t CH = kHtT * kHtKPT;
+  const uint32_t nbig = (uint32_t)plan[kPlanBig];
+  const uint32_t total = (uint32_t)plan[kPlanBigT];
+  const uint64_t cap = plan[kPlanCap];
+  __shared__ uint32_t s_j;
+  for (uint32_t c0 = blockIdx.x * CH; c0 < total; c0 += gridDim.x * CH) {
+    if (threadIdx.x == 0) s_j = upper_index(big_t, nbig, c0);
+    __syncthreads();
+    const uint32_t j0 = s_j;
+    __syncthreads();
+    const uint32_t e0 = c0 + threadIdx.x * kHtKPT;
+    K cur = K(0);
+    uint32_t run = 0;
+    for (int u = 0; u < kHtKPT; u++) {
+      const uint32_t e = e0 + u;
+      bool flush = false;
+      K key = K(0);
+      if (e < total) {
+        const uint32_t j = e >= big_t[j0 + 1] ? j0 + 1 : j0;  // j0 < nbig
+        const uint32_t tb = t_off[min((uint64_t)big_bin[j] << s, v)];
+        key = t_edges[tb + (e - big_t[j])];
+        if (run && key != cur) flush = true;
+      }
+      // flush the finished run (warp peers with the same key merge into one add)
+      const uint32_t fm = __ballot_sync(0xffffffffu, flush);
+      if (flush) {
+        const uint32_t peers = __match_any_sync(fm, cur);
+        const uint32_t sum = __reduce_add_sync(peers, run);
+        if ((peers & lanemask_lt()) == 0) ht_add(hk, hc, cap, cur, sum, plan + kPlanOnes);
+        run = 0;
+      }
+      if (e < total) {
+        cur = key;
+        run++;
+      }
+    }
+    const bool last = run != 0;
+    const uint32_t lm = __ballot_sync(0xffffffffu, last);
+    if (last) {
+      const uint32_t peers = __match_any_sync(lm, cur);
+      const uint32_t sum = __reduce_add_sync(peers, run);
+      if ((peers & lanemask_lt()) == 0) ht_add(hk, hc, cap, cur, sum, plan + kPlanOnes);
+    }
+  }
+}
+
+// Queries of the hash-table bins, flattened; results go to the bin-ordered
+// multiplicities like the shared-memory probe's.
+template <typename H>
+__global__ void __launch_bounds__(kHtT) k_ht_lookup(const KeyOf<H>* __restrict__ qpart, const uint32_t* __restrict__ q_start,
+                                                    const uint32_t* __restrict__ t_off, HashParams hp, int s, uint64_t v,
+                                                    const uint32_t* __restrict__ big_bin, const uint32_t* __restrict__ big_q,
+                                                    const unsigned long long* __restrict__ plan, const KeyOf<H>* __restrict__ hk,
+                                                    const uint32_t* __restrict__ hc, uint32_t* __restrict__ mult_bo,
+                                                    unsigned long long* __restrict__ agg) {
+  using K = KeyOf<H>;
+  constexpr uint32_t CH = kHtT * 4;
+  const uint32_t nbig = (uint32_t)plan[kPlanBig];
+  const uint32_t total = (uint32_t)plan[kPlanBigQ];
+  const uint64_t cap = plan[kPlanCap];
+  const uint32_t ones = (uint32_t)plan[kPlanOnes];
+  __shared__ uint32_t s_j[2];
+  uint64_t matched = 0, tot = 0, comps = 0;
+  for (uint32_t c0 = blockIdx.x * CH; c0 < total; c0 += gridDim.x * CH) {
+    if (threadIdx.x == 0) s_j[0] = upper_index(big_q, nbig, c0);
+    if (threadIdx.x == 1) s_j[1] = upper_index(big_q, nbig, min(total, c0 + CH) - 1);
+    __syncthreads();
+    const uint32_t ja = s_j[0], jz = s_j[1];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t e = c0 + u * kHtT + threadIdx.x;
+      if (e < total) {
+        uint32_t a = ja, z = jz + 1;  // big_q[a] <= e < big_q[z]
+        while (z - a > 1) {
+          const uint32_t m = (a + z) >> 1;
+          if (big_q[m] <= e) a = m; else z = m;
+        }
+        const uint32_t pos = q_start[big_bin[a]] + (e - big_q[a]);
+        const K q = qpart[pos];
+        const uint32_t h = H::bucket(q, hp);
+        const uint32_t c = ht_count(hk, hc, cap, q, ones);
+        mult_bo[pos] = c;
+        matched += c != 0;
+        tot += c;
+        comps += t_off[(uint64_t)h + 1] - t_off[h];
+      }
+    }
+  }
+  flush_agg(matched, tot, comps, agg);
+}

@@ -1172,8 +1172,16 @@ __device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32
 }
 
 // ---- small per-CTA map for deep buckets (high-duplicate inputs)
-constexpr uint32_t kBigDeg = 16;     // buckets deeper than this use the map
-constexpr uint32_t kMapSlots = 256;  // open addressing, power of two
+// Bucket depth classes of the shared-memory probe.  d <= 4: four branch-free
+// slots; d <= kLinDeg: the slots plus a short warp-uniform linear tail;
+// d <= kSortMax: the bucket is sorted in smem at staging and the count is
+// upper_bound - lower_bound (O(log d) per query, like the reference's
+// searchsorted, query.py:104-117); deeper: the per-bin key -> count map.
+constexpr uint32_t kLinDeg = 8;
+constexpr uint32_t kSortMax = 1024;
+constexpr uint32_t kBigDeg = kSortMax;  // buckets deeper than this use the map
+constexpr uint32_t kMapSlots = 256;     // open addressing, power of two
+enum : uint32_t { kBinSort = 1, kBinMap = 2 };  // depth classes present in a bin
 
 template <typename K>
 struct BigMap {
@@ -1243,39 +1251,7 @@ __device__ __noinline__ uint32_t map_count(const BigMap<K>& m, K key) {
   return 0;
 }
 
-// Slices above the smem capacity: the bin's queries, 16 per thread per batch,
-// each answered by IntersectArray over its bucket in global memory or by the
-// deep-bucket map.
-template <typename H>
-__device__ __forceinline__ void probe_queries_global(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
-                                                     const HashParams& hp, const uint32_t* __restrict__ t_off,
-                                                     const KeyOf<H>* __restrict__ t_edges, const BigMap<KeyOf<H>>& map,
-                                                     bool overflow, uint32_t* __restrict__ mult_bo,
-                                                     KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
-                                                     uint64_t& comps) {
-  using K = typename H::Key;
-  constexpr int QPT = kProbeQPT;
-  for (uint32_t q0 = qlo; q0 < qhi; q0 += QPT * kT) {
-    if (q0 != qlo) load_queries<K>(qpart, q0, qhi, qv);
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t j = q0 + k * kT + threadIdx.x;
-      if (j < qhi) {
-        const K q = qv[k];
-        const uint32_t h = H::bucket(q, hp);
-        const uint32_t a = t_off[h], e = t_off[h + 1];
-        uint32_t c = 0;
-        if (e - a > kBigDeg && !overflow) c = map_count(map, q);
-        else
-          for (uint32_t t = a; t < e; t++) c += (t_edges[t] == q);
-        mult_bo[j] = c;
-        matched += (c != 0);
-        total += c;
-        comps += e - a;
-      }
-    }
-  }
-}
+#include "hg_bigbin.cuh"
 
 // The bin's queries against the staged slice, 16 per thread per batch (the
 // loads were issued first), in phases so the hashes, offset loads and slot
@@ -1287,12 +1263,13 @@ __device__ __forceinline__ void probe_queries_global(const KeyOf<H>* __restrict_
 // deepest bucket rather than a divergent per-lane loop.  Buckets deeper than
 // kBigDeg are answered from the map (one warp-uniform check per batch).
 // One batch (QPT queries per thread): kFull -- every query slot of the batch
-// is valid, so no bounds checks; bin_deep -- the bin has buckets deeper than
-// kBigDeg (known from staging), only then are queries checked for the map.
+// is valid, so no bounds checks; bin_flags -- which depth classes the bin has
+// (known from staging): only then are queries checked for the sorted search
+// or the map.
 template <typename H, bool kFull>
 __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const HashParams& hp, uint32_t first,
                                             const uint16_t* off16, const KeyOf<H>* te, const BigMap<KeyOf<H>>& map,
-                                            bool overflow, bool bin_deep, uint32_t* __restrict__ mult_bo,
+                                            bool overflow, uint32_t bin_flags, uint32_t* __restrict__ mult_bo,
                                             const KeyOf<H> (&qv)[kProbeQPT], uint32_t& m32, uint32_t& t32,
                                             uint32_t& d32) {
   using K = typename H::Key;
@@ -1309,7 +1286,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
     }
   }
   bool deep = false;
-  if (bin_deep) {
+  if (bin_flags & kBinMap) {
 #pragma unroll
     for (int k = 0; k < QPT; k++) deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
   }
@@ -1320,14 +1297,45 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
     const K q = qv[k];
     const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
     const bool mapped = use_map && d > kBigDeg;
+    const bool srt = (bin_flags & kBinSort) && d > kLinDeg && d <= kSortMax;
     const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
     uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
                  (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
-    const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped ? 0u : d);
+    const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped || srt ? 0u : d);
     for (uint32_t t = 4; t < dmax; t++) {
       const bool in = t < d;
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
+    }
+    if (bin_flags & kBinSort) {
+      // sorted bucket: lower and upper bound in one warp-uniform loop of
+      // floor(log2(max d)) + 1 steps (two independent search chains)
+      const uint32_t smax = __reduce_max_sync(0xffffffffu, srt ? d : 0u);
+      if (smax) {
+        uint32_t lb = a, ln = srt ? d : 0u, ub = a, un = ln;
+        const int steps = 32 - __clz(smax);
+        for (int it = 0; it < steps; it++) {
+          const uint32_t hl = ln >> 1, hu = un >> 1;
+          const K xl = te[lb + hl], xu = te[ub + hu];
+          if (ln) {
+            if (xl < q) {
+              lb += hl + 1;
+              ln -= hl + 1;
+            } else {
+              ln = hl;
+            }
+          }
+          if (un) {
+            if (!(q < xu)) {
+              ub += hu + 1;
+              un -= hu + 1;
+            } else {
+              un = hu;
+            }
+          }
+        }
+        if (srt) c = ub - lb;
+      }
     }
     if (use_map && mapped) c = map_count(map, q);
     const uint32_t j = q0 + k * kT + threadIdx.x;
@@ -1344,7 +1352,7 @@ template <typename H>
 __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
                                                    const HashParams& hp, uint32_t first, const uint16_t* off16,
                                                    const KeyOf<H>* te, const BigMap<KeyOf<H>>& map, bool overflow,
-                                                   bool bin_deep, uint32_t* __restrict__ mult_bo,
+                                                   uint32_t bin_flags, uint32_t* __restrict__ mult_bo,
                                                    KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
                                                    uint64_t& comps) {
   using K = typename H::Key;
@@ -1358,52 +1366,105 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
     }
     if (q0 + B < qhi) load_queries<K>(qpart, q0 + B, qhi, qn);
     uint32_t m32 = 0, t32 = 0, d32 = 0;
-    if (qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_deep, mult_bo, qv, m32, t32, d32);
-    else probe_batch<H, false>(q0, qhi, hp, first, off16, te, map, overflow, bin_deep, mult_bo, qv, m32, t32, d32);
+    if (qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
+    else probe_batch<H, false>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
     matched += m32;
     total += t32;
     comps += d32;
   }
 }
 
-// One CTA per fine bin: the table's CSR slice (uint16 local offsets + edges)
-// staged in smem; the bin's queries probe it with IntersectArray semantics
-// (count of equal keys in the bucket; comparisons += bucket
-// degree, query.py:153-155) and write counts in partitioned order.  Slices
-// above the smem capacity are probed in global memory.
+// Sort one bucket of d keys (kLinDeg < d <= kSortMax) in smem, by one warp.
+// d <= 32: a register bitonic network over shuffles (the all-ones sentinel
+// pads to 32 and sorts last).  Larger: the bitonic network in place with the
+// mirror form of each merge, so every comparator is ascending and the
+// virtual +inf elements past d never move (pairs reaching past d are skipped).
+template <typename K>
+__device__ __forceinline__ void warp_sort_bucket(K* p, uint32_t d, int lane) {
+  if (d <= 32) {
+    K x = (uint32_t)lane < d ? p[lane] : ~K(0);
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const K y = __shfl_xor_sync(0xffffffffu, x, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        x = (lower == up) ? (y < x ? y : x) : (y < x ? x : y);
+      }
+    }
+    if ((uint32_t)lane < d) p[lane] = x;
+    __syncwarp();
+    return;
+  }
+  const uint32_t P = 1u << (32 - __clz(d - 1));
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const int lj = __ffs(j) - 1;
+      for (uint32_t t = lane; t < P / 2; t += 32) {
+        const uint32_t blk = t >> lj, x = t & (j - 1);
+        uint32_t lo, hi;
+        if (j == (k >> 1)) {
+          lo = blk * k + x;
+          hi = blk * k + k - 1 - x;
+        } else {
+          lo = blk * 2 * j + x;
+          hi = lo + j;
+        }
+        if (hi < d) {
+          const K u = p[lo], w = p[hi];
+          if (w < u) {
+            p[lo] = w;
+            p[hi] = u;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Shared-memory probe work item = (fine bin, chunk of <= kProbeChunk of its
+// queries); bins whose table slice exceeds kCap take the hash-table path
+// (hg_bigbin.cuh) and have no items.  The table's CSR slice (uint16 local
+// offsets + edges) is staged in smem; the queries probe it with
+// IntersectArray semantics (count of equal keys in the bucket, PAPER.md:62-72;
+// comparisons += bucket degree, query.py:153-155) and write counts in
+// partitioned order.  Hot bins split into several items, so a skewed query
+// set does not serialise on one SM.
 template <typename H>
 __global__ void __launch_bounds__(kT, 2)
 k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t_edges, const KeyOf<H>* __restrict__ qpart,
-              const uint32_t* __restrict__ q_start, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ mult_bo,
-              unsigned long long* __restrict__ agg) {
+              const uint32_t* __restrict__ q_start, const uint32_t* __restrict__ item_bin,
+              const unsigned long long* __restrict__ plan, HashParams hp, int s, uint64_t v,
+              uint32_t* __restrict__ mult_bo, unsigned long long* __restrict__ agg) {
   using K = typename H::Key;
   constexpr uint32_t VPL = 16 / sizeof(K);
-  constexpr uint32_t kCap = LocalShape<K>::kCap;
   extern __shared__ __align__(128) unsigned char s_raw[];
   __shared__ alignas(8) uint64_t s_bar;
-  __shared__ uint32_t s_deep;
+  __shared__ uint32_t s_flags;
+  constexpr uint32_t kCap = LocalShape<K>::kCap;
+  if (blockIdx.x >= plan[kPlanItems]) return;
   const uint32_t S = 1u << s;
   uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);                        // S + 1 (+ pad to 8)
   K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 8
   BigMap<K>& map = *reinterpret_cast<BigMap<K>*>(reinterpret_cast<unsigned char*>(tedges) + (kCap + 8) * sizeof(K));
-  const uint32_t f = blockIdx.x;
-  const uint32_t qlo = q_start[f];
-  uint32_t qhi = q_start[f + 1];
-  if (qlo == qhi) return;
+  const uint32_t it = item_bin[blockIdx.x];
+  const uint32_t f = it & 0x7FFFu;
+  const uint32_t qlo = q_start[f] + (it >> 15) * kProbeChunk;
+  uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
   K qv[kProbeQPT];
   load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
-  const uint32_t tn = thi - tlo;
-  const bool in_smem = tn <= kCap;
+  const uint32_t tn = thi - tlo;  // <= kCap (the plan sends larger slices to the hash table)
   // edges: one TMA bulk copy of the 16-byte chunks from the boundary below
   // tlo (tedges[sh + j] = edge tlo + j) lands while the offsets convert
   const uint32_t a0 = tlo & ~(VPL - 1);
-  const uint32_t sh = in_smem ? tlo - a0 : 0u;
-  const uint32_t ebytes = in_smem ? ((thi - a0) * (uint32_t)sizeof(K) + 15u) & ~15u : 0u;
+  const uint32_t sh = tlo - a0;
+  const uint32_t ebytes = tn ? ((thi - a0) * (uint32_t)sizeof(K) + 15u) & ~15u : 0u;
   if (threadIdx.x == 0) {
-    s_deep = in_smem ? 0u : 1u;
+    s_flags = 0;
     if (ebytes) {
       mbar_init(&s_bar, 1);
       fence_proxy_async();
@@ -1411,12 +1472,12 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
     }
   }
   map_clear(map);
-  if (in_smem) {
+  {
     // offsets: 4 per 16-byte load (first is a multiple of 2^s), stored as u16
-    // relative to tlo, three loads in flight per thread; also flag the bin if
-    // any bucket is deeper than kBigDeg
+    // relative to tlo, three loads in flight per thread; the bin's depth
+    // classes (sorted / map) are flagged on the way
     const uint4* o4 = reinterpret_cast<const uint4*>(t_off + first);
-    bool deep = false;
+    uint32_t flags = 0;
     constexpr int R = 3;
     for (uint32_t w0 = threadIdx.x; 4 * w0 <= nb; w0 += R * blockDim.x) {
       uint4 x[R];
@@ -1440,29 +1501,57 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
         const uint32_t w = w0 + r * blockDim.x, i0 = 4 * w;
         if (i0 > nb) break;
         // degrees of buckets i0..i0+3 (only those below nb exist)
-        deep |= (i0 + 1 <= nb && x[r].y - x[r].x > kBigDeg) | (i0 + 2 <= nb && x[r].z - x[r].y > kBigDeg) |
-                (i0 + 3 <= nb && x[r].w - x[r].z > kBigDeg) | (i0 + 4 <= nb && nx[r] - x[r].w > kBigDeg);
+        const uint32_t dg[4] = {i0 + 1 <= nb ? x[r].y - x[r].x : 0u, i0 + 2 <= nb ? x[r].z - x[r].y : 0u,
+                                i0 + 3 <= nb ? x[r].w - x[r].z : 0u, i0 + 4 <= nb ? nx[r] - x[r].w : 0u};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          flags |= dg[e] > kBigDeg ? (uint32_t)kBinMap : 0u;
+          flags |= (dg[e] > kLinDeg && dg[e] <= kSortMax) ? (uint32_t)kBinSort : 0u;
+        }
         const uint32_t lo2 = ((x[r].x - tlo) & 0xFFFFu) | ((x[r].y - tlo) << 16);
         const uint32_t hi2 = ((x[r].z - tlo) & 0xFFFFu) | ((x[r].w - tlo) << 16);
         reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
       }
     }
-    __syncthreads();  // s_deep initialised
-    if (__any_sync(0xffffffffu, deep) && (threadIdx.x & 31) == 0) s_deep = 1u;
+    __syncthreads();  // s_flags initialised
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (flags && (threadIdx.x & 31) == 0) atomicOr(&s_flags, flags);
     if (threadIdx.x == 0 && ebytes) mbar_wait(&s_bar, 0);
   }
   __syncthreads();
-  const K* te = tedges + sh;
+  const uint32_t bin_flags = s_flags;
+  K* te = tedges + sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (bin_flags & kBinSort) {
+    // every warp scans its share of the buckets and sorts the ones in the
+    // sorted class, one at a time (buckets are disjoint between warps)
+    const uint32_t per = ((nb + nw - 1) / nw + 31) & ~31u;
+    const uint32_t b1 = min(nb, (uint32_t)(warp + 1) * per);
+    for (uint32_t b0 = warp * per; b0 < b1; b0 += 32) {
+      const uint32_t l = b0 + lane;
+      uint32_t a = 0, d = 0;
+      if (l < b1) {
+        a = off16[l];
+        d = (uint32_t)off16[l + 1] - a;
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, d > kLinDeg && d <= kSortMax);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        warp_sort_bucket<K>(te + __shfl_sync(0xffffffffu, a, src), __shfl_sync(0xffffffffu, d, src), lane);
+      }
+    }
+    __syncthreads();
+  }
   // Buckets deeper than kBigDeg (high-duplicate inputs) are answered from a
   // small smem map key -> occurrences, built once per bin, instead of an
   // O(degree) scan per query (the map was cleared before staging).
-  if (s_deep) {
+  if (bin_flags & kBinMap) {
     // All warps walk the slice's edges (warp w owns a contiguous range of
     // 32-edge rows; lane j sees every 32nd edge of it).  Each lane counts runs
     // of equal keys and adds a run to the map when its key changes, so a deep
     // bucket holding one repeated key costs a few map updates spread over the
     // whole CTA instead of one warp-serial update per 32 keys.
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t rows = (tn + 31) / 32;
     const uint32_t per = (rows + nw - 1) / nw;
     const uint32_t r1 = min(rows, (uint32_t)(warp + 1) * per);
@@ -1472,14 +1561,13 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
     for (uint32_t r = (uint32_t)warp * per; r < r1; r++) {
       const uint32_t t = r * 32 + lane;
       if (t >= tn) break;
-      const K key = in_smem ? te[t] : t_edges[tlo + t];
+      const K key = te[t];
       if (run == 0 || key != cur) {
         if (run && cur_deep) map_add_n(map, cur, run);
         cur = key;
         run = 0;
         const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
-        const uint32_t d = in_smem ? (uint32_t)off16[l + 1] - off16[l] : t_off[first + l + 1] - t_off[first + l];
-        cur_deep = d > kBigDeg;
+        cur_deep = (uint32_t)off16[l + 1] - off16[l] > kBigDeg;
       }
       run++;
     }
@@ -1491,11 +1579,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
 #if defined(HG_EXP_PROBE) && HG_EXP_PROBE == 3  // timing experiment (tools/build_variant.py): first batch only
   qhi = min(qhi, qlo + kProbeQPT * kT);
 #endif
-  if (in_smem)
-    probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, s_deep != 0, mult_bo, qv,
-                          matched, total, comps);
-  else
-    probe_queries_global<H>(qpart, qlo, qhi, hp, t_off, t_edges, map, overflow, mult_bo, qv, matched, total, comps);
+  probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, bin_flags, mult_bo, qv, matched,
+                        total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
 }
 
@@ -1511,7 +1596,18 @@ static size_t probe_smem(int s, int key_bits) {
 }
 static size_t unpart_smem() { return (2 * kUnpStaged + 2 * (kMaxBins + 1) + 2 * kMaxBins + kMaxBins + 1) * 4 + 16; }
 
-size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query) {
+// Hash-table slots the query reserves for oversized bins: a bin exceeds the
+// smem capacity only if the table has more keys than that capacity; the
+// device sizes the live table to >= 2x the keys of the bins that take it.
+static uint64_t ht_slots(uint64_t n_table, int key_bits) {
+  const uint64_t cap = key_bits == 32 ? LocalShape<uint32_t>::kCap : LocalShape<uint64_t>::kCap;
+  if (n_table <= cap) return 0;
+  uint64_t c = 1024;
+  while (c < 2 * n_table) c <<= 1;
+  return c;
+}
+
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query, uint64_t n_table) {
   const size_t kb = key_bits / 8;
   size_t b = 0;
   b += align_up((size_t)L.grid * L.nb1 * 4, 256);        // M
@@ -1524,8 +1620,13 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query)
     b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
     b += align_up(L.max_tiles2 * (2 * kSub + 1) * 4, 256);  // meta2
     b += align_up(n * 4 + 16, 256);                      // bin-ordered multiplicities (+ tail padding)
+    b += align_up((L.nfine + n / kProbeChunk + 1) * 4, 256);  // probe items
+    b += 3 * align_up(((size_t)L.nfine + 1) * 4, 256);   // big bins, their table / query prefixes
+    b += align_up(kPlanWords * 8, 256);                  // plan
+    const uint64_t hs = ht_slots(n_table, key_bits);
+    b += align_up(hs * kb, 256) + align_up(hs * 4, 256);  // hash table keys + counts
   } else {
-    b += align_up((size_t)num_sms() * (1u << L.s) * 4, 256);  // big-bin scratch
+    b += align_up(((size_t)L.nfine + 1) * 4, 256);       // oversized-bin chunk prefix
   }
   return b + 4096;
 }
@@ -1619,38 +1720,69 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   PartOut po{};
   int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
   if (rc) return rc;
-  uint32_t* scratch = ws.take<uint32_t>((size_t)num_sms() * (1u << L.s));
+  uint32_t* big_cp = ws.take<uint32_t>(L.nfine + 1);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
   const size_t smC = LocalPShape<K>::smem(L.s);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
   HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
             L.nfine, hp, L.s, v, offsets, edges);
-  // oversized fine bins: with two levels their keys sit in edges (in place), so
-  // they are copied to the free level-1 buffer first
+  // oversized fine bins (hg_bigbin.cuh), in chunks over the whole grid: with
+  // two levels their keys sit in edges (in place), so the count pass copies
+  // them to the free level-1 buffer and placement reads them from there
+  K* src = (K*)po.out1;
   const int copy = L.two_level ? 1 : 0;
   const size_t smBig = (size_t)(1u << L.s) * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_big<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
-  HG_LAUNCH("hg_local_build_big", k_local_build_big<H>, num_sms(), 1024, smBig, st, (K*)po.out1, copy, po.fine_start,
-            po.big_list, po.big_count, hp, L.s, v, scratch, offsets, edges);
+  HG_LAUNCH("hg_big_plan", k_big_plan<K>, 1, 1024, 0, st, po.fine_start, po.big_list, po.big_count, big_cp);
+  HG_LAUNCH("hg_big_zero", k_big_zero, num_sms(), 256, 0, st, po.big_list, po.big_count, L.s, v, offsets);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_count<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, src, copy, po.fine_start, po.big_list,
+            po.big_count, big_cp, hp, L.s, v, offsets);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_LAUNCH("hg_big_scan", k_big_scan, num_sms(), 1024, smBig, st, po.fine_start, po.big_list, po.big_count, L.s, v,
+            offsets);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, po.big_list,
+            po.big_count, big_cp, hp, L.s, v, offsets, edges);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_LAUNCH("hg_big_fix", k_big_fix, num_sms(), 1024, smBig, st, po.fine_start, po.big_list, po.big_count, L.s, v,
+            offsets);
   return HG_OK;
 }
 
 template <typename H>
-static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyOf<H>* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
-                 cudaEvent_t split) {
+static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n_table, const KeyOf<H>* queries, uint64_t q,
+                      const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws,
+                      cudaStream_t st, cudaEvent_t split) {
   using K = KeyOf<H>;
   PartOut po{};
   int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
   if (rc) return rc;
   if (split) HG_CHECK_CUDA(cudaEventRecord(split, st));  // query-side grouping done (intersect_timed's split)
   uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
+  const uint32_t max_items = (uint32_t)(L.nfine + q / kProbeChunk + 1);
+  uint32_t* item_bin = ws.take<uint32_t>(max_items);
+  uint32_t* big_bin = ws.take<uint32_t>(L.nfine + 1);
+  uint32_t* big_t = ws.take<uint32_t>(L.nfine + 1);
+  uint32_t* big_q = ws.take<uint32_t>(L.nfine + 1);
+  unsigned long long* plan = ws.take<unsigned long long>(kPlanWords);
+  const uint64_t hs = ht_slots(n_table, sizeof(K) * 8);
+  K* hk = ws.take<K>(hs);
+  uint32_t* hc = ws.take<uint32_t>(hs);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
+  HG_LAUNCH("hg_probe_plan", k_probe_plan, 1, 1024, 0, st, t_off, po.fine_start, L.nfine, L.s, v,
+            LocalShape<K>::kCap, item_bin, big_bin, big_t, big_q, plan);
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
-  HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
-            po.fine_start, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  HG_LAUNCH("hg_local_probe", k_local_probe<H>, max_items, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
+            po.fine_start, item_bin, plan, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  if (hs) {  // oversized table slices: key -> count hash table over the whole grid
+    HG_LAUNCH("hg_ht_clear", k_ht_clear<K>, num_sms() * 4, 256, 0, st, plan, hk, hc);
+    HG_LAUNCH("hg_ht_insert", k_ht_insert<H>, num_sms() * 2, kHtT, 0, st, t_off, t_edges, L.s, v, big_bin, big_t, plan, hk,
+              hc);
+    HG_LAUNCH("hg_ht_lookup", k_ht_lookup<H>, num_sms() * 2, kHtT, 0, st, (const K*)po.grouped, po.fine_start, t_off, hp,
+              L.s, v, big_bin, big_q, plan, hk, hc, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  }
   const size_t smR = unpart_smem();
   uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
   if (L.two_level) {
@@ -1698,11 +1830,11 @@ int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, co
 }
 
 template <typename K>
-int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
-                 cudaEvent_t split) {
+int binned_query(const uint32_t* t_off, const K* t_edges, uint64_t n_table, const K* queries, uint64_t q,
+                 const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws,
+                 cudaStream_t st, cudaEvent_t split) {
   return with_hasher<K>(hp, [&](auto h) {
-    return query_impl<decltype(h)>(t_off, t_edges, queries, q, hp, v, L, mult, agg, ws, st, split);
+    return query_impl<decltype(h)>(t_off, t_edges, n_table, queries, q, hp, v, L, mult, agg, ws, st, split);
   });
 }
 
@@ -1710,11 +1842,11 @@ template int binned_build<uint32_t>(const uint32_t*, uint64_t, const HashParams&
                                     uint32_t*, uint32_t*, Workspace&, cudaStream_t);
 template int binned_build<uint64_t>(const uint64_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
                                     uint32_t*, uint64_t*, Workspace&, cudaStream_t);
-template int binned_query<uint32_t>(const uint32_t*, const uint32_t*, const uint32_t*, uint64_t, const HashParams&,
-                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t,
-                                    cudaEvent_t);
-template int binned_query<uint64_t>(const uint32_t*, const uint64_t*, const uint64_t*, uint64_t, const HashParams&,
-                                    uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&, cudaStream_t,
-                                    cudaEvent_t);
+template int binned_query<uint32_t>(const uint32_t*, const uint32_t*, uint64_t, const uint32_t*, uint64_t,
+                                    const HashParams&, uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&,
+                                    cudaStream_t, cudaEvent_t);
+template int binned_query<uint64_t>(const uint32_t*, const uint64_t*, uint64_t, const uint64_t*, uint64_t,
+                                    const HashParams&, uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&,
+                                    cudaStream_t, cudaEvent_t);
 
 }  // namespace hg

@@ -20,13 +20,13 @@ struct BinLayout {
 };
 
 bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L);
-size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query);
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query, uint64_t n_table = 0);
 template <typename K>
 int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
                  K* edges, Workspace& ws, cudaStream_t st);
 template <typename K>
-int binned_query(const uint32_t* t_off, const K* t_edges, const K* queries, uint64_t q, const HashParams& hp,
-                 uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws, cudaStream_t st,
-                 cudaEvent_t split = nullptr);
+int binned_query(const uint32_t* t_off, const K* t_edges, uint64_t n_table, const K* queries, uint64_t q,
+                 const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws,
+                 cudaStream_t st, cudaEvent_t split = nullptr);
 
 }  // namespace hg

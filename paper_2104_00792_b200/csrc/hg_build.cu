@@ -343,16 +343,11 @@ int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const uint32_t*
                                   hp, mult, agg, s);
 }
 
-size_t hg_query_workspace_size(uint64_t q, uint64_t v, int key_bits) {
+size_t hg_query_workspace_size(uint64_t q, uint64_t v, uint64_t n_table, int key_bits) {
   size_t kb = key_bits / 8;
   size_t b = align_up(4 * (v + 1), 256) + align_up(kb * q, 256) + align_up(4 * q, 256) + build_ws_bytes(q, v, key_bits) + 1024;
-  // The binned layout depends on the table's keys per bucket (more keys per
-  // bucket -> smaller fine bins -> more of them -> more workspace), which this
-  // query does not know: size for every table density the binned path accepts.
-  for (int lg = 0; lg <= 16; lg++) {
-    BinLayout L;
-    if (use_binned(v << lg, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true));
-  }
+  BinLayout L;
+  if (use_binned(n_table, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true, n_table));
   return b;
 }
 
@@ -365,12 +360,12 @@ static int query_entry(const uint32_t* offsets_a, const void* edges_a, uint64_t 
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
   BinLayout L;
-  if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, true) <= workspace_bytes) {
+  if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, true, n_a) <= workspace_bytes) {
     if (key_bits == 32)
-      return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)queries, q, hp, v, L, mult,
-                                    agg, ws, s, split);
-    return binned_query<uint64_t>(offsets_a, (const uint64_t*)edges_a, (const uint64_t*)queries, q, hp, v, L, mult,
-                                  agg, ws, s, split);
+      return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, n_a, (const uint32_t*)queries, q, hp, v, L,
+                                    mult, agg, ws, s, split);
+    return binned_query<uint64_t>(offsets_a, (const uint64_t*)edges_a, n_a, (const uint64_t*)queries, q, hp, v, L,
+                                  mult, agg, ws, s, split);
   }
   size_t kb = key_bits / 8;
   uint32_t* qoff = ws.take<uint32_t>(v + 1);

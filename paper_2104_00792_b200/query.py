@@ -155,7 +155,7 @@ def query_device(table: HashGraph, queries_dev):
             queries_dev = queries_dev.to(table.keys_device.device)
         mult = t.empty(q, dtype=t.int32, device=queries_dev.device)
         agg = t.zeros(3, dtype=t.int64, device=queries_dev.device)
-        ws = D.workspace(_lib.load().hg_query_workspace_size(q, table.hash_range, table.key_bits))
+        ws = D.workspace(_lib.load().hg_query_workspace_size(q, table.hash_range, table.num_keys, table.key_bits))
         _lib.call("hg_query", D.ptr(table.offset_device), D.ptr(table.keys_device), table.num_keys,
                   D.ptr(queries_dev), q, table.key_bits, kind, seed, table.hash_range, D.ptr(mult), D.ptr(agg),
                   D.ptr(ws), ws.numel(), D.stream_ptr())
@@ -226,7 +226,7 @@ def _intersect_timed_device(ta, queries):
     mult = t.zeros(nb, dtype=t.int32, device=qd.device)
     agg = t.zeros(3, dtype=t.int64, device=qd.device)
     kind, seed = family_code(ta.family)
-    ws = D.workspace(_lib.load().hg_query_workspace_size(nb, ta.hash_range, ta.key_bits))
+    ws = D.workspace(_lib.load().hg_query_workspace_size(nb, ta.hash_range, ta.num_keys, ta.key_bits))
     ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[1].record()  # creates the split event; the library re-records it at the split point
     ev[0].record()

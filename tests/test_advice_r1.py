@@ -83,7 +83,7 @@ def test_query_agg_accumulates_on_every_path():
         qd = D.to_device_keys(O.generate_keys(20, n, 0x51), 32)
         agg = torch.zeros(3, dtype=torch.int64, device="cuda")
         mult = torch.empty(n, dtype=torch.int32, device="cuda")
-        ws = D.workspace(_lib.load().hg_query_workspace_size(n, table.hash_range, 32))
+        ws = D.workspace(_lib.load().hg_query_workspace_size(n, table.hash_range, table.num_keys, 32))
         for _ in range(2):
             _lib.call("hg_query", D.ptr(table.offset_device), D.ptr(table.keys_device), table.num_keys, D.ptr(qd), n,
                       32, 0, 0, table.hash_range, D.ptr(mult), D.ptr(agg), D.ptr(ws), ws.numel(), D.stream_ptr())

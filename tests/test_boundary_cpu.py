@@ -35,7 +35,7 @@ def test_library_exports_every_header_symbol():
 def test_workspace_queries_are_host_only():
     lib = _lib.load()
     assert lib.hg_build_workspace_size(1 << 20, 1 << 20, 32) >= 4 * (1 << 20)
-    assert lib.hg_query_workspace_size(1 << 20, 1 << 20, 32) > lib.hg_build_workspace_size(1 << 20, 1 << 20, 32)
+    assert lib.hg_query_workspace_size(1 << 20, 1 << 20, 1 << 20, 32) > lib.hg_build_workspace_size(1 << 20, 1 << 20, 32)
     assert lib.hg_reorganize_workspace_size(1 << 20, 8) > 0
 
 

@@ -1,0 +1,160 @@
+"""Skewed and high-duplicate inputs through the CUDA path vs the CPU oracle (GPU only).
+
+The reference's intersection is O(log d) per query whatever the bucket depth
+(searchsorted on a (bucket, key)-sorted copy, query.py:102-117), and its
+acceptance suite sweeps the duplicate rate (test_acceptance.py:160-196).
+These cases drive every depth class of the shared-memory probe (four slots,
+linear tail, sorted buckets + binary search, per-bin map), the hash-table
+path for fine bins too large for shared memory, hot bins split over several
+probe work items, and the multi-CTA build of oversized bins.  Parity rules as
+everywhere: offsets exact, buckets equal as multisets (canonical),
+multiplicities and matched/total/comparisons exact.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+hg = pytest.importorskip("paper_2104_00792_b200")
+
+
+def check(keys, queries, hash_range=None, key_bits=32):
+    v = int(hash_range) if hash_range else O.hash_range_for(len(keys), 1.0)
+    table = hg.build(keys, 1.0, hash_range=v, key_bits=key_bits)
+    off, placed, _ = O.build_csr(keys, v, workers=O.default_workers())
+    assert np.array_equal(table.offset, off)
+    assert np.array_equal(O.canonical(table.offset, table.keys)[1], O.canonical(off, placed)[1])
+    res = hg.intersect(table, queries)
+    mult, matched, total, comp, _ = O.query(off, placed, queries, workers=O.default_workers())
+    assert np.array_equal(res.multiplicities, mult)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
+    return table, res
+
+
+def zipf_keys(n, seed, a=1.1, key_bits=32):
+    """Pareto-discretised Zipf(a): key = floor(u^(-1/(a-1))) mod 2^bits."""
+    u = np.random.default_rng(seed).random(n)
+    x = np.floor(np.maximum(u, 1e-300) ** (-1.0 / (a - 1.0)))
+    x = np.mod(x, 2.0 ** min(key_bits, 53)).astype(np.uint64)
+    return x.astype(np.uint32) if key_bits == 32 else x * np.uint64(0x9E3779B97F4A7C15)
+
+
+N = 1 << 20
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 12, 16, 32, 64, 128, 256, 1024, 1 << 14, 1 << 20])
+def test_duplicate_rate_sweep(d):
+    """acceptance c05/c06 shapes: hash range N / d, d keys per bucket on average."""
+    keys = O.generate_keys(20, N, 0)
+    queries = O.generate_keys(20, N, 0x51)
+    check(keys, queries, hash_range=max(1, N // d))
+
+
+@pytest.mark.parametrize("d", [1, 16, 128, 1 << 12])
+def test_duplicate_rate_sweep_u64(d):
+    keys = O.generate_keys(32, N, 0, key_bits=64)
+    queries = np.concatenate([keys[::3], O.generate_keys(32, N // 2, 0x51, key_bits=64)])
+    check(keys, queries, hash_range=max(1, N // d), key_bits=64)
+
+
+def test_all_identical():
+    keys = np.full(N, 7, dtype=np.uint32)
+    queries = np.concatenate([np.full(N // 2, 7, np.uint32), O.generate_keys(20, N // 2, 0x51)])
+    table, res = check(keys, queries)
+    assert res.matched_positions >= N // 2 and res.total_matches >= (N // 2) * N
+
+
+def test_identical_queries_uniform_table():
+    """Every query lands in one fine bin: the bin's queries are split over many
+    probe work items."""
+    keys = O.generate_keys(20, N, 0)
+    queries = np.full(N, int(keys[12345]), dtype=np.uint32)
+    check(keys, queries)
+
+
+def test_half_identical_mixture():
+    keys = O.generate_keys(20, N, 3)
+    keys[::2] = 0xDEADBEEF
+    queries = np.concatenate([keys[:N // 4], O.generate_keys(20, N // 2, 0x51)])
+    check(keys, queries)
+
+
+def test_all_ones_key_in_hash_table_path():
+    """0xFFFFFFFF is the hash table's empty marker: it is counted separately."""
+    keys = O.generate_keys(20, N, 5)
+    keys[: N // 2] = 0xFFFFFFFF
+    keys[N // 2: N // 2 + 1000] = 0
+    queries = np.concatenate([np.array([0xFFFFFFFF, 0, 1, 0xFFFFFFFE], np.uint32), keys[::7]])
+    check(keys, queries, hash_range=64)
+
+
+def test_all_ones_key_u64():
+    keys = O.generate_keys(32, N, 5, key_bits=64)
+    keys[: N // 2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    queries = np.concatenate([np.array([0xFFFFFFFFFFFFFFFF, 0, 1], np.uint64), keys[::7]])
+    check(keys, queries, hash_range=256, key_bits=64)
+
+
+@pytest.mark.parametrize("a", [1.1, 1.5])
+def test_zipf(a):
+    keys = zipf_keys(N, 11, a)
+    queries = np.concatenate([zipf_keys(N // 2, 12, a), O.generate_keys(20, N // 2, 0x51)])
+    check(keys, queries)
+
+
+def test_zipf_u64():
+    keys = zipf_keys(N, 11, 1.1, key_bits=64)
+    queries = zipf_keys(N, 12, 1.1, key_bits=64)
+    check(keys, queries, key_bits=64)
+
+
+def test_identity_hash_structured_deep_buckets():
+    """Identity hash with multiples of V: every key of a residue class lands in
+    one bucket (deep sorted buckets with many distinct keys)."""
+    v = 1 << 12
+    keys = (np.arange(N, dtype=np.uint64) * v % (1 << 32)).astype(np.uint32)
+    keys = np.concatenate([keys[: N // 2], O.generate_keys(32, N // 2, 9)])
+    queries = np.concatenate([keys[::5], O.generate_keys(32, N // 4, 0x51)])
+    fam = hg.HashFamily(hg.HashKind.IDENTITY, 0)
+    table = hg.build(keys, 1.0, family=fam, hash_range=v)
+    off, placed, _ = O.build_csr(keys, v, kind=O.KIND_IDENTITY)
+    assert np.array_equal(table.offset, off)
+    assert np.array_equal(O.canonical(table.offset, table.keys)[1], O.canonical(off, placed)[1])
+    res = hg.intersect(table, queries)
+    mult, matched, total, comp, _ = O.query(off, placed, queries, kind=O.KIND_IDENTITY)
+    assert np.array_equal(res.multiplicities, mult)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
+
+
+def test_sorted_bucket_depth_boundaries():
+    """Identity hash, V = 2^16, ~2^20 keys (fine bins of 1024 buckets that fit
+    shared memory): bucket 1024 * i holds 17 * i keys (depths 0..1071, so the
+    4 / 8 / 1024 class boundaries all occur), every other bucket 15 keys,
+    bucket 1 holds 3000 distinct keys (map class; the map overflows: linear
+    fallback) and bucket 1026 holds 2000 copies of five keys (map class).
+    Queries hit present and absent keys of every bucket."""
+    v = 1 << 16
+    rng = np.random.default_rng(77)
+    depth = np.full(v, 15, dtype=np.int64)
+    depth[::1024] = np.arange(v // 1024) * 17
+    depth[1] = 3000
+    depth[1026] = 0
+    owner = np.repeat(np.arange(v, dtype=np.uint64), depth)
+    keys = rng.integers(0, 1 << 16, size=len(owner), dtype=np.uint64) * v + owner
+    keys = np.concatenate([keys, np.repeat(np.arange(5, dtype=np.uint64) * v + 1026, 400)])
+    keys = (keys % (1 << 32)).astype(np.uint32)
+    keys = keys[rng.permutation(len(keys))]
+    queries = np.concatenate([keys[::3], keys[::5] + np.uint32(v),
+                              rng.integers(0, 1 << 32, 4096, dtype=np.uint64).astype(np.uint32)])
+    fam = hg.HashFamily(hg.HashKind.IDENTITY, 0)
+    table = hg.build(keys, 1.0, family=fam, hash_range=v)
+    off, placed, _ = O.build_csr(keys, v, kind=O.KIND_IDENTITY)
+    assert np.array_equal(table.offset, off)
+    assert np.array_equal(O.canonical(table.offset, table.keys)[1], O.canonical(off, placed)[1])
+    res = hg.intersect(table, queries)
+    mult, matched, total, comp, _ = O.query(off, placed, queries, kind=O.KIND_IDENTITY)
+    assert np.array_equal(res.multiplicities, mult)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
