@@ -1,6 +1,6 @@
 // hg_bigbin.cuh -- fine bins too large for shared memory (high-duplicate and
-// skewed inputs).  Part of hg_binned.cu (included there after its block
-// helpers); split out for size.
+// skewed inputs).  Part of hg_binned.cu (textually included inside its
+// namespace hg, after its block helpers); split out for size.
 //
 // A fine bin holds more than kCap keys only when many keys share few buckets:
 // all-identical keys, Zipf-like hot keys, or a hash range far below the key
@@ -9,63 +9,21 @@
 // Such a bin must not serialise on one SM, so both sides work in chunks that
 // every CTA of the grid shares:
 //
-//   build   k_big_plan   chunk prefix over the oversized bins
-//           k_big_zero   zero their bucket counters (= the offsets slice)
-//           k_big_count  per chunk: smem counts, one global add per bucket
-//           k_big_scan   per bin: counts -> bucket starts (in offsets)
+//   build   k_starts     lists the oversized bins, their chunk prefix
+//           k_local_build_p  zeroes their bucket counters (= the offsets slice)
+//           k_big_count  per chunk: smem counts, one global add per bucket;
+//                        the CTA finishing a bin's last chunk turns its
+//                        counts into bucket starts
 //           k_big_place  per chunk: smem ranks, one global claim per bucket,
-//                        keys stored at claim + rank
-//           k_big_fix    per bin: claimed ends -> starts (shift by one)
-//   query   k_probe_plan per fine bin: shared-memory probe work items, or the
-//                        hash-table path when the table slice is oversized
-//           k_ht_clear   key -> count table (open addressing) for those bins
+//                        keys stored at claim + rank; the CTA finishing a
+//                        bin's last chunk shifts the claimed ends to starts
+//   query   k_probe_plan per fine bin: extra probe work items for hot bins,
+//                        the list of bins whose table slice is oversized
+//           k_ht_prep    key -> count hash table for those bins (cleared),
+//                        their table-key / query prefixes
 //           k_ht_insert  their table keys, runs and warp peers aggregated
 //           k_ht_lookup  their queries: count from the table, comparisons
 //                        from the bucket degree (query.py:153-155)
-// (no include guard / namespace: textually included inside hg_binned.cu's namespace hg)
-
-// Block-wide exclusive scan of one value per thread (any blockDim <= 1024);
-// returns the exclusive prefix, `total` gets the block sum.  Three barriers.
-template <typename T>
-__device__ __forceinline__ T block_scan_excl(T x, T& total) {
-  __shared__ T s_ws[33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  T inc = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const T y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) s_ws[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const T w = lane < nw ? s_ws[lane] : T(0);
-    T wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const T y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
-    }
-    s_ws[lane] = wi - w;
-    if (lane == 31) s_ws[32] = wi;
-  }
-  __syncthreads();
-  const T r = s_ws[warp] + inc - x;
-  total = s_ws[32];
-  __syncthreads();
-  return r;
-}
-
-// Index j with pre[j] <= x < pre[j + 1] (pre ascending, pre[0] = 0, n entries + end).
-__device__ __forceinline__ uint32_t upper_index(const uint32_t* pre, uint32_t n, uint32_t x) {
-  uint32_t a = 0, z = n;
-  while (z - a > 1) {
-    const uint32_t m = (a + z) >> 1;
-    if (pre[m] <= x) a = m; else z = m;
-  }
-  return a;
-}
-
 // ============================================================================ build
 
 template <typename K>
@@ -75,41 +33,7 @@ struct BigShape {
   static constexpr uint32_t kChunk = kKPT * kThreads;
 };
 
-// One CTA: big_cp[j] = chunks before oversized bin j; big_cp[nbig] = total.
-template <typename K>
-__global__ void __launch_bounds__(1024) k_big_plan(const uint32_t* __restrict__ fine_start,
-                                                   const uint32_t* __restrict__ big_list,
-                                                   const uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_cp) {
-  constexpr uint32_t CH = BigShape<K>::kChunk;
-  const uint32_t nbig = *big_count;
-  uint32_t carry = 0;
-  for (uint32_t base = 0; base < nbig; base += blockDim.x) {
-    const uint32_t j = base + threadIdx.x;
-    uint32_t c = 0;
-    if (j < nbig) {
-      const uint32_t f = big_list[j];
-      c = (fine_start[f + 1] - fine_start[f] + CH - 1) / CH;
-    }
-    uint32_t tot;
-    const uint32_t e = block_scan_excl<uint32_t>(c, tot);
-    if (j < nbig) big_cp[j] = carry + e;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) big_cp[nbig] = carry;
-}
-
-// Bucket counters of the oversized bins live in their offsets slice: zero it.
-__global__ void k_big_zero(const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count, int s,
-                           uint64_t v, uint32_t* __restrict__ offsets) {
-  const uint32_t nbig = *big_count;
-  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
-    const uint64_t first = (uint64_t)big_list[j] << s;
-    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
-    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = 0;
-  }
-}
-
-// Locate chunk k: bin index j, fine bin f, key range [lo, hi).
+// Locate chunk k: bin index j, fine bin f, key range [lo, hi), chunks of j.
 __device__ __forceinline__ void big_chunk(uint32_t k, uint32_t nbig, uint32_t CH, const uint32_t* __restrict__ big_cp,
                                           const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ fine_start,
                                           uint32_t* s_loc) {
@@ -120,29 +44,51 @@ __device__ __forceinline__ void big_chunk(uint32_t k, uint32_t nbig, uint32_t CH
     s_loc[0] = f;
     s_loc[1] = lo;
     s_loc[2] = min(fine_start[f + 1], lo + CH);
+    s_loc[3] = j;
+    s_loc[4] = big_cp[j + 1] - big_cp[j];
   }
   __syncthreads();
 }
 
+// True in every thread of the CTA that completed the last of `nchunks`
+// chunks of bin j (done[j] counts completed chunks; zeroed by k_starts).
+// The CTA's global writes and atomics are fenced before the count, and the
+// winner fences again before it reads the others' results.
+__device__ __forceinline__ bool last_chunk(uint32_t* done, uint32_t j, uint32_t nchunks) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done + j, 1u) == nchunks - 1;
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
 // Per chunk: count keys per bucket in smem (lanes of a warp that hit the same
 // bucket share one atomic), then add the nonzero counters to the bin's global
-// counters.  `copy` (two partition levels: the grouped keys sit in `edges`)
-// also copies the chunk to `dst` so placement can overwrite edges.
+// counters (its offsets slice, zeroed by k_local_build_p).  The CTA that
+// completes a bin's last chunk scans the counts into bucket starts.  `copy`
+// (two partition levels: the grouped keys sit in `edges`) also copies the
+// chunk to `dst` so placement can overwrite edges.
 template <typename H>
 __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__ src, KeyOf<H>* __restrict__ dst, int copy,
                                                     const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
                                                     const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_cp,
-                                                    HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets) {
+                                                    uint32_t* __restrict__ done, HashParams hp, int s, uint64_t v,
+                                                    uint32_t* __restrict__ offsets) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
-  __shared__ uint32_t s_loc[3];
+  __shared__ uint32_t s_loc[5];
   const uint32_t nbig = *big_count;
+  if (nbig == 0) return;
   const uint32_t nch = big_cp[nbig];
   const uint32_t lt = lanemask_lt();
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
     big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
-    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2];
+    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2], j = s_loc[3], nck = s_loc[4];
     const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
     for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = 0;
@@ -150,14 +96,14 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
     K kv[BS::kKPT];
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
-      kv[u] = j < hi ? src[j] : K(0);
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
-      const bool ok = j < hi;
-      if (ok && copy) dst[j] = kv[u];
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = e < hi;
+      if (ok && copy) dst[e] = kv[u];
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
       if (ok && (peers & lt) == 0) atomicAdd(cnt + l, (uint32_t)__popc(peers));
@@ -165,70 +111,58 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
     __syncthreads();
     for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x)
       if (cnt[l]) atomicAdd(offsets + first + l, cnt[l]);
-    __syncthreads();
-  }
-}
-
-// Per oversized bin: counts -> bucket starts (exclusive scan + the bin's first key).
-__global__ void __launch_bounds__(1024) k_big_scan(const uint32_t* __restrict__ fine_start,
-                                                   const uint32_t* __restrict__ big_list,
-                                                   const uint32_t* __restrict__ big_count, int s, uint64_t v,
-                                                   uint32_t* __restrict__ offsets) {
-  extern __shared__ uint32_t a[];  // 2^s
-  const uint32_t nbig = *big_count;
-  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
-    const uint32_t f = big_list[j];
-    const uint64_t first = (uint64_t)f << s;
-    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
-    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) a[l] = offsets[first + l];
-    __syncthreads();
-    block_exscan_rows(a, nb, fine_start[f]);
-    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = a[l];
+    if (last_chunk(done, j, nck)) {
+      for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = __ldcg(offsets + first + l);
+      __syncthreads();
+      block_exscan_rows(cnt, nb, fine_start[f]);
+      for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = cnt[l];
+    }
     __syncthreads();
   }
 }
 
 // Per chunk: ranks from smem counters (warp peers share one atomic), one
 // global claim per nonzero bucket (the offsets slice is the cursor), then
-// every key stored at claim + rank.  Bucket order inside a bucket is free
-// (core.py:12-14).
+// every key stored at claim + rank; in-bucket order is free (core.py:12-14).
+// After a bin's last chunk every cursor holds its bucket's end = the next
+// bucket's start; the CTA that completed it shifts them back by one bucket.
 template <typename H>
 __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__ src, const uint32_t* __restrict__ fine_start,
                                                     const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count,
-                                                    const uint32_t* __restrict__ big_cp, HashParams hp, int s, uint64_t v,
-                                                    uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges) {
+                                                    const uint32_t* __restrict__ big_cp, uint32_t* __restrict__ done,
+                                                    HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets,
+                                                    KeyOf<H>* __restrict__ edges) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
-  __shared__ uint32_t s_loc[3];
+  __shared__ uint32_t s_loc[5];
   const uint32_t nbig = *big_count;
+  if (nbig == 0) return;
   const uint32_t nch = big_cp[nbig];
   const uint32_t lt = lanemask_lt();
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
     big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
-    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2];
+    const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2], j = s_loc[3], nck = s_loc[4];
     const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
     for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = 0;
     __syncthreads();
     K kv[BS::kKPT];
-    uint32_t lr[BS::kKPT];  // bucket << 16 | rank would overflow: bucket (<= 14 bits) and rank (< 2^17) packed below
+    uint32_t lr[BS::kKPT];  // bucket << 15 | rank (bucket < 2^14, rank < kChunk <= 2^14)
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
-      kv[u] = j < hi ? src[j] : K(0);
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t j = lo + u * BS::kThreads + threadIdx.x;
-      const bool ok = j < hi;
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = e < hi;
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
-      const int leader = __ffs(peers) - 1;
       uint32_t b0 = 0;
       if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
-      b0 = __shfl_sync(0xffffffffu, b0, leader);
-      // rank < kChunk <= 2^14 fits 15 bits; bucket < 2^s <= 2^14 fits 17 bits
+      b0 = __shfl_sync(0xffffffffu, b0, __ffs(peers) - 1);
       lr[u] = ok ? (l << 15) | (b0 + __popc(peers & lt)) : 0xFFFFFFFFu;
     }
     __syncthreads();
@@ -240,110 +174,43 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++)
       if (lr[u] != 0xFFFFFFFFu) edges[cnt[lr[u] >> 15] + (lr[u] & 0x7FFFu)] = kv[u];
-    __syncthreads();
-  }
-}
-
-// Per oversized bin: after placement every cursor holds its bucket's end, i.e.
-// the next bucket's start; shift by one bucket.
-__global__ void __launch_bounds__(1024) k_big_fix(const uint32_t* __restrict__ fine_start,
-                                                  const uint32_t* __restrict__ big_list,
-                                                  const uint32_t* __restrict__ big_count, int s, uint64_t v,
-                                                  uint32_t* __restrict__ offsets) {
-  extern __shared__ uint32_t a[];  // 2^s
-  const uint32_t nbig = *big_count;
-  for (uint32_t j = blockIdx.x; j < nbig; j += gridDim.x) {
-    const uint32_t f = big_list[j];
-    const uint64_t first = (uint64_t)f << s;
-    const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
-    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) a[l] = offsets[first + l];
-    __syncthreads();
-    for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = l ? a[l - 1] : fine_start[f];
+    if (last_chunk(done, j, nck)) {
+      for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = __ldcg(offsets + first + l);
+      __syncthreads();
+      for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) offsets[first + l] = l ? cnt[l - 1] : fine_start[f];
+    }
     __syncthreads();
   }
 }
 
 // ============================================================================ query
 
-// plan words (uint64): items, big bins, big table keys, big queries, hash-table capacity, all-ones-key count
+// plan words (uint64, zeroed by k_starts): extra probe items, hash-table bins,
+// their table keys, their queries, hash-table capacity, all-ones-key count
 enum : int { kPlanItems = 0, kPlanBig, kPlanBigT, kPlanBigQ, kPlanCap, kPlanOnes, kPlanWords };
 constexpr uint32_t kProbeChunk = 32768;  // queries per shared-memory probe work item
 
-// One CTA.  Fine bin f: tn table keys (t_off at the bin's bucket boundaries),
-// qn queries.  tn <= cap: ceil(qn / kProbeChunk) probe items (item_bin =
-// f | chunk << 15).  tn > cap and qn > 0: the hash-table path (big_bin,
-// big_t / big_q = prefixes of table keys / queries over those bins).
-// Each thread owns a contiguous run of bins; loads are issued before the scan.
-__global__ void __launch_bounds__(1024) k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t* __restrict__ q_start,
-                                                     uint32_t nfine, int s, uint64_t v, uint32_t cap,
-                                                     uint32_t* __restrict__ item_bin, uint32_t* __restrict__ big_bin,
-                                                     uint32_t* __restrict__ big_t, uint32_t* __restrict__ big_q,
-                                                     unsigned long long* __restrict__ plan) {
-  const uint32_t per = (nfine + blockDim.x - 1) / blockDim.x;
-  const uint32_t f0 = min(nfine, threadIdx.x * per), f1 = min(nfine, f0 + per);
-  auto tab = [&](uint32_t f) -> uint32_t { return t_off[min((uint64_t)f << s, v)]; };
-  // pass 1: per-thread sums (items, big bins, big table keys, big queries)
-  uint32_t si = 0, sb = 0, st = 0, sq = 0;
-  if (f0 < f1) {
-    uint32_t ta = tab(f0), qa = q_start[f0];
-    for (uint32_t f = f0; f < f1; f++) {
-      const uint32_t tb = tab(f + 1), qb = q_start[f + 1];
-      const uint32_t tn = tb - ta, qn = qb - qa;
-      if (qn) {
-        if (tn <= cap) si += (qn + kProbeChunk - 1) / kProbeChunk;
-        else {
-          sb++;
-          st += tn;
-          sq += qn;
-        }
-      }
-      ta = tb;
-      qa = qb;
-    }
-  }
-  uint32_t ti, tb_, tt, tq;
-  uint32_t ei = block_scan_excl<uint32_t>(si, ti);
-  uint32_t eb = block_scan_excl<uint32_t>(sb, tb_);
-  uint32_t et = block_scan_excl<uint32_t>(st, tt);
-  uint32_t eq = block_scan_excl<uint32_t>(sq, tq);
-  // pass 2: write (the loads hit L1/L2 now)
-  if (f0 < f1) {
-    uint32_t ta = tab(f0), qa = q_start[f0];
-    for (uint32_t f = f0; f < f1; f++) {
-      const uint32_t tb = tab(f + 1), qb = q_start[f + 1];
-      const uint32_t tn = tb - ta, qn = qb - qa;
-      if (qn) {
-        if (tn <= cap) {
-          const uint32_t k = (qn + kProbeChunk - 1) / kProbeChunk;
-          for (uint32_t c = 0; c < k; c++) item_bin[ei + c] = f | (c << 15);
-          ei += k;
-        } else {
-          big_bin[eb] = f;
-          big_t[eb] = et;
-          big_q[eb] = eq;
-          eb++;
-          et += tn;
-          eq += qn;
-        }
-      }
-      ta = tb;
-      qa = qb;
-    }
-  }
-  if (threadIdx.x == 0) {
-    big_t[tb_] = tt;
-    big_q[tb_] = tq;
-    plan[kPlanItems] = ti;
-    plan[kPlanBig] = tb_;
-    plan[kPlanBigT] = tt;
-    plan[kPlanBigQ] = tq;
-    unsigned long long c = 0;
-    if (tt) {
-      c = 1024;
-      while (c < 2ull * tt) c <<= 1;
-    }
-    plan[kPlanCap] = c;
-    plan[kPlanOnes] = 0;
+// One thread per fine bin f with queries (tn table keys, qn queries).  A bin
+// whose table slice fits smem is probed by CTA f (its first kProbeChunk
+// queries) plus one extra work item per further chunk (item = f | c << 15);
+// a larger slice goes to the hash-table path (big_bin list).  List order is
+// free: every consumer works from the lists as written.
+__global__ void k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t* __restrict__ q_start, uint32_t nfine,
+                             int s, uint64_t v, uint32_t cap, uint32_t* __restrict__ item_x, uint32_t* __restrict__ big_bin,
+                             unsigned long long* __restrict__ plan) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfine) return;
+  const uint32_t qn = q_start[f + 1] - q_start[f];
+  if (qn == 0) return;
+  const uint32_t tn = t_off[min((uint64_t)(f + 1) << s, v)] - t_off[(uint64_t)f << s];
+  if (tn > cap) {
+    big_bin[atomicAdd(plan + kPlanBig, 1ull)] = f;
+    atomicAdd(plan + kPlanBigT, (unsigned long long)tn);
+    atomicAdd(plan + kPlanBigQ, (unsigned long long)qn);
+  } else if (qn > kProbeChunk) {
+    const uint32_t k = (qn + kProbeChunk - 1) / kProbeChunk;
+    const uint32_t base = (uint32_t)atomicAdd(plan + kPlanItems, (unsigned long long)(k - 1));
+    for (uint32_t c = 1; c < k; c++) item_x[base + c - 1] = f | (c << 15);
   }
 }
 
@@ -352,12 +219,51 @@ __device__ __forceinline__ uint64_t ht_slot(K key) {
   return fmix64((uint64_t)key * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull);
 }
 
+__device__ __forceinline__ unsigned long long ht_capacity(unsigned long long keys) {
+  if (!keys) return 0;
+  unsigned long long c = 1024;
+  while (c < 2 * keys) c <<= 1;
+  return c;
+}
+
+// Clear the hash table (capacity = pow2 >= 2x the keys of the hash-table
+// bins); CTA 0 also writes the per-bin table-key / query prefixes.
 template <typename K>
-__global__ void k_ht_clear(const unsigned long long* __restrict__ plan, K* __restrict__ hk, uint32_t* __restrict__ hc) {
-  const uint64_t cap = plan[kPlanCap];
+__global__ void k_ht_prep(unsigned long long* __restrict__ plan, const uint32_t* __restrict__ big_bin,
+                          const uint32_t* __restrict__ t_off, const uint32_t* __restrict__ q_start, int s, uint64_t v,
+                          uint32_t* __restrict__ big_t, uint32_t* __restrict__ big_q, K* __restrict__ hk,
+                          uint32_t* __restrict__ hc) {
+  const uint32_t nbig = (uint32_t)plan[kPlanBig];
+  if (nbig == 0) return;
+  const unsigned long long cap = ht_capacity(plan[kPlanBigT]);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
     hk[i] = ~K(0);
     hc[i] = 0;
+  }
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x == 0) plan[kPlanCap] = cap;
+  uint32_t ct = 0, cq = 0;
+  for (uint32_t base = 0; base < nbig; base += blockDim.x) {
+    const uint32_t j = base + threadIdx.x;
+    uint32_t tn = 0, qn = 0;
+    if (j < nbig) {
+      const uint32_t f = big_bin[j];
+      tn = t_off[min((uint64_t)(f + 1) << s, v)] - t_off[(uint64_t)f << s];
+      qn = q_start[f + 1] - q_start[f];
+    }
+    uint32_t tt, tq;
+    const uint32_t et = block_scan_excl<uint32_t>(tn, tt);
+    const uint32_t eq = block_scan_excl<uint32_t>(qn, tq);
+    if (j < nbig) {
+      big_t[j] = ct + et;
+      big_q[j] = cq + eq;
+    }
+    ct += tt;
+    cq += tq;
+  }
+  if (threadIdx.x == 0) {
+    big_t[nbig] = ct;
+    big_q[nbig] = cq;
   }
 }
 
@@ -416,6 +322,7 @@ __global__ void __launch_bounds__(kHtT) k_ht_insert(const uint32_t* __restrict__
   using K = KeyOf<H>;
   constexpr uint32_t CH = kHtT * kHtKPT;
   const uint32_t nbig = (uint32_t)plan[kPlanBig];
+  if (nbig == 0) return;
   const uint32_t total = (uint32_t)plan[kPlanBigT];
   const uint64_t cap = plan[kPlanCap];
   __shared__ uint32_t s_j;
@@ -472,6 +379,7 @@ __global__ void __launch_bounds__(kHtT) k_ht_lookup(const KeyOf<H>* __restrict__
   using K = KeyOf<H>;
   constexpr uint32_t CH = kHtT * 4;
   const uint32_t nbig = (uint32_t)plan[kPlanBig];
+  if (nbig == 0) return;
   const uint32_t total = (uint32_t)plan[kPlanBigQ];
   const uint64_t cap = plan[kPlanCap];
   const uint32_t ones = (uint32_t)plan[kPlanOnes];

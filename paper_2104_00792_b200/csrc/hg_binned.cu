@@ -177,6 +177,48 @@ __device__ uint32_t block_exscan_rows(uint32_t* a, uint32_t n, uint32_t base) {
   return total;
 }
 
+// Block-wide exclusive scan of one value per thread (any blockDim <= 1024);
+// returns the exclusive prefix, `total` gets the block sum.  Three barriers.
+template <typename T>
+__device__ __forceinline__ T block_scan_excl(T x, T& total) {
+  __shared__ T s_ws[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  T inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < nw ? s_ws[lane] : T(0);
+    T wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    s_ws[lane] = wi - w;
+    if (lane == 31) s_ws[32] = wi;
+  }
+  __syncthreads();
+  const T r = s_ws[warp] + inc - x;
+  total = s_ws[32];
+  __syncthreads();
+  return r;
+}
+
+// Index j with pre[j] <= x < pre[j + 1] (pre ascending, pre[0] = 0, n entries + end).
+__device__ __forceinline__ uint32_t upper_index(const uint32_t* pre, uint32_t n, uint32_t x) {
+  uint32_t a = 0, z = n;
+  while (z - a > 1) {
+    const uint32_t m = (a + z) >> 1;
+    if (pre[m] <= x) a = m; else z = m;
+  }
+  return a;
+}
+
 __device__ __forceinline__ uint32_t get16(const uint32_t* p, uint32_t k) { return (p[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu; }
 
 // Tile loads: full 16-byte-aligned tiles use 128-bit loads (element of key k
@@ -297,12 +339,18 @@ __global__ void __launch_bounds__(1024) k_colscan(uint32_t* __restrict__ M, uint
 }
 
 // One CTA: fine starts (F+1), level-1 starts (nb1+1), level-2 tile prefix
-// (nb1+1; tp[nb1] = level-2 tile count), fine cursors (= fine starts) and the
-// list of fine bins above `cap` keys.
+// (nb1+1; tp[nb1] = level-2 tile count), fine cursors (= fine starts), the
+// list of fine bins above `cap` keys with its prefix of `big_chunk`-key chunks
+// (big_cp, nbig+1) and zeroed per-bin chunk-completion counters (big_done[j]
+// and big_done[nfine + 1 + j], j < nbig), and `nzero` zeroed words at `zero`
+// (the query's plan).
 __global__ void __launch_bounds__(1024)
 k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, uint32_t nb1, uint32_t tile,
          uint32_t cap, uint32_t* __restrict__ fine_start, uint32_t* __restrict__ c_start, uint32_t* __restrict__ tp,
-         uint32_t* __restrict__ fine_cursor, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
+         uint32_t* __restrict__ fine_cursor, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count,
+         uint32_t big_chunk, uint32_t* __restrict__ big_cp, uint32_t* __restrict__ big_done, uint32_t* __restrict__ zero,
+         uint32_t nzero) {
+  for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0;
   extern __shared__ uint32_t s_a[];  // nfine + nb1 + 1
   __shared__ uint32_t s_big;
   uint32_t* s_t = s_a + nfine;
@@ -334,6 +382,28 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
   const uint32_t ntiles = block_exscan(s_t, nb1);
   for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) tp[c] = s_t[c];
   if (threadIdx.x == 0) tp[nb1] = ntiles;
+  // oversized bins (hg_bigbin.cuh): chunk prefix, completion counters
+  const uint32_t nbig = s_big;
+  if (big_cp == nullptr || nbig == 0) return;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nbig; base += blockDim.x) {
+    const uint32_t j = base + threadIdx.x;
+    uint32_t c = 0;
+    if (j < nbig) {
+      const uint32_t f = big_list[j];
+      const uint32_t hi = f + 1 < nfine ? s_a[f + 1] : total;
+      c = (hi - s_a[f] + big_chunk - 1) / big_chunk;
+    }
+    uint32_t tot;
+    const uint32_t e = block_scan_excl<uint32_t>(c, tot);
+    if (j < nbig) big_cp[j] = carry + e;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) big_cp[nbig] = carry;
+  for (uint32_t j = threadIdx.x; j < nbig; j += blockDim.x) {
+    big_done[j] = 0;              // k_big_count
+    big_done[nfine + 1 + j] = 0;  // k_big_place
+  }
 }
 
 // --------------------------------------------------------------------------- partition
@@ -930,8 +1000,15 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
   K* raw = reinterpret_cast<K*>(s_raw + PS::c16_bytes(s));            // next bin's keys (TMA)
   K* staged = raw + PS::kElems;                                       // this bin's edges, chunk-aligned to global
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets[v] = fine_start[nfine];
-  auto next_small = [&](uint32_t f) -> uint32_t {  // bins above kCap belong to k_local_build_big
-    while (f < nfine && fine_start[f + 1] - fine_start[f] > kCap) f += gridDim.x;
+  // bins above kCap belong to k_big_count / k_big_place; their bucket
+  // counters (the offsets slice) are zeroed here
+  auto next_small = [&](uint32_t f) -> uint32_t {
+    while (f < nfine && fine_start[f + 1] - fine_start[f] > kCap) {
+      const uint64_t fb = (uint64_t)f << s;
+      const uint32_t nbz = (uint32_t)min((uint64_t)S, v - fb);
+      for (uint32_t l = threadIdx.x; l < nbz; l += NT) offsets[fb + l] = 0;
+      f += gridDim.x;
+    }
     return f;
   };
   // bin f's keys [lo, hi) land at raw[lo - lo_al ...] with one bulk copy of
@@ -1177,7 +1254,7 @@ __device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32
 // d <= kSortMax: the bucket is sorted in smem at staging and the count is
 // upper_bound - lower_bound (O(log d) per query, like the reference's
 // searchsorted, query.py:104-117); deeper: the per-bin key -> count map.
-constexpr uint32_t kLinDeg = 8;
+constexpr uint32_t kLinDeg = 16;
 constexpr uint32_t kSortMax = 1024;
 constexpr uint32_t kBigDeg = kSortMax;  // buckets deeper than this use the map
 constexpr uint32_t kMapSlots = 256;     // open addressing, power of two
@@ -1424,8 +1501,9 @@ __device__ __forceinline__ void warp_sort_bucket(K* p, uint32_t d, int lane) {
 }
 
 // Shared-memory probe work item = (fine bin, chunk of <= kProbeChunk of its
-// queries); bins whose table slice exceeds kCap take the hash-table path
-// (hg_bigbin.cuh) and have no items.  The table's CSR slice (uint16 local
+// queries): CTA f takes bin f's first chunk, CTAs past nfine the further
+// chunks of hot bins (k_probe_plan); bins whose table slice exceeds kCap take
+// the hash-table path (hg_bigbin.cuh).  The table's CSR slice (uint16 local
 // offsets + edges) is staged in smem; the queries probe it with
 // IntersectArray semantics (count of equal keys in the bucket, PAPER.md:62-72;
 // comparisons += bucket degree, query.py:153-155) and write counts in
@@ -1434,7 +1512,7 @@ __device__ __forceinline__ void warp_sort_bucket(K* p, uint32_t d, int lane) {
 template <typename H>
 __global__ void __launch_bounds__(kT, 2)
 k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t_edges, const KeyOf<H>* __restrict__ qpart,
-              const uint32_t* __restrict__ q_start, const uint32_t* __restrict__ item_bin,
+              const uint32_t* __restrict__ q_start, uint32_t nfine, const uint32_t* __restrict__ item_x,
               const unsigned long long* __restrict__ plan, HashParams hp, int s, uint64_t v,
               uint32_t* __restrict__ mult_bo, unsigned long long* __restrict__ agg) {
   using K = typename H::Key;
@@ -1443,21 +1521,28 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   __shared__ alignas(8) uint64_t s_bar;
   __shared__ uint32_t s_flags;
   constexpr uint32_t kCap = LocalShape<K>::kCap;
-  if (blockIdx.x >= plan[kPlanItems]) return;
   const uint32_t S = 1u << s;
   uint16_t* off16 = reinterpret_cast<uint16_t*>(s_raw);                        // S + 1 (+ pad to 8)
   K* tedges = reinterpret_cast<K*>(s_raw + ((2 * (S + 8) + 15) & ~15u));       // VPL + kCap + 8
   BigMap<K>& map = *reinterpret_cast<BigMap<K>*>(reinterpret_cast<unsigned char*>(tedges) + (kCap + 8) * sizeof(K));
-  const uint32_t it = item_bin[blockIdx.x];
-  const uint32_t f = it & 0x7FFFu;
-  const uint32_t qlo = q_start[f] + (it >> 15) * kProbeChunk;
+  uint32_t f = blockIdx.x, c = 0;  // CTA f: the first chunk of bin f's queries
+  if (f >= nfine) {                // further chunks of hot bins
+    const uint32_t x = f - nfine;
+    if (x >= plan[kPlanItems]) return;
+    const uint32_t it = item_x[x];
+    f = it & 0x7FFFu;
+    c = it >> 15;
+  }
+  const uint32_t qlo = q_start[f] + c * kProbeChunk;
   uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
+  if (qlo >= qhi) return;
   K qv[kProbeQPT];
   load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
-  const uint32_t tn = thi - tlo;  // <= kCap (the plan sends larger slices to the hash table)
+  const uint32_t tn = thi - tlo;
+  if (tn > kCap) return;  // the hash-table path answers this bin (k_ht_lookup)
   // edges: one TMA bulk copy of the 16-byte chunks from the boundary below
   // tlo (tedges[sh + j] = edge tlo + j) lands while the offsets convert
   const uint32_t a0 = tlo & ~(VPL - 1);
@@ -1620,13 +1705,14 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query,
     b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
     b += align_up(L.max_tiles2 * (2 * kSub + 1) * 4, 256);  // meta2
     b += align_up(n * 4 + 16, 256);                      // bin-ordered multiplicities (+ tail padding)
-    b += align_up((L.nfine + n / kProbeChunk + 1) * 4, 256);  // probe items
-    b += 3 * align_up(((size_t)L.nfine + 1) * 4, 256);   // big bins, their table / query prefixes
+    b += align_up((n / kProbeChunk + 1) * 4, 256);     // extra probe items
+    b += 3 * align_up(((size_t)L.nfine + 1) * 4, 256);   // hash-table bins, their table / query prefixes
     b += align_up(kPlanWords * 8, 256);                  // plan
     const uint64_t hs = ht_slots(n_table, key_bits);
     b += align_up(hs * kb, 256) + align_up(hs * 4, 256);  // hash table keys + counts
   } else {
     b += align_up(((size_t)L.nfine + 1) * 4, 256);       // oversized-bin chunk prefix
+    b += align_up(((size_t)L.nfine + 1) * 8, 256);       // their chunk-completion counters
   }
   return b + 4096;
 }
@@ -1634,6 +1720,9 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query,
 struct PartOut {
   const void* grouped;  // keys grouped by fine bin at fine_start positions
   void* out1;           // level-1 buffer (n keys of workspace)
+  uint32_t* big_cp;     // build: oversized-bin chunk prefix (nfine + 1)
+  uint32_t* big_done;   // build: their chunk-completion counters (2 x nfine)
+  uint32_t* plan32;     // query: the probe plan words (zeroed by k_starts)
   uint32_t* M;
   uint32_t* fine_start;
   uint32_t* c_start;
@@ -1660,6 +1749,9 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   po->tp = ws.take<uint32_t>(L.nb1 + 1);
   po->big_count = ws.take<uint32_t>(64);
   po->M = ws.take<uint32_t>((size_t)L.grid * L.nb1);
+  po->big_cp = query ? nullptr : ws.take<uint32_t>(L.nfine + 1);
+  po->big_done = query ? nullptr : ws.take<uint32_t>(2 * (size_t)L.nfine + 2);
+  po->plan32 = query ? ws.take<uint32_t>(2 * kPlanWords) : nullptr;
   K* out1 = ws.take<K>(n + 16 / sizeof(K));  // + tail padding for k_part2's TMA
   K* out2 = nullptr;
   po->out1 = out1;
@@ -1685,7 +1777,8 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   const size_t smS = ((size_t)L.nfine + L.nb1 + 1) * 4;
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smS));
   HG_LAUNCH("hg_starts", k_starts, 1, 1024, smS, st, fine_cnt, L.nfine, L.group, L.nb1, L.tile, cap, po->fine_start,
-            po->c_start, po->tp, fine_cursor, po->big_list, po->big_count);
+            po->c_start, po->tp, fine_cursor, po->big_list, po->big_count, (uint32_t)BigShape<K>::kChunk, po->big_cp,
+            po->big_done, po->plan32, po->plan32 ? (uint32_t)(2 * kPlanWords) : 0u);
   const size_t smP = part_smem(sizeof(K) * 8);
   if (query) {
     HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
@@ -1720,8 +1813,6 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   PartOut po{};
   int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
   if (rc) return rc;
-  uint32_t* big_cp = ws.take<uint32_t>(L.nfine + 1);
-  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
   const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
   const size_t smC = LocalPShape<K>::smem(L.s);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
@@ -1733,20 +1824,12 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   K* src = (K*)po.out1;
   const int copy = L.two_level ? 1 : 0;
   const size_t smBig = (size_t)(1u << L.s) * 4;
-  HG_LAUNCH("hg_big_plan", k_big_plan<K>, 1, 1024, 0, st, po.fine_start, po.big_list, po.big_count, big_cp);
-  HG_LAUNCH("hg_big_zero", k_big_zero, num_sms(), 256, 0, st, po.big_list, po.big_count, L.s, v, offsets);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_count<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
   HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, src, copy, po.fine_start, po.big_list,
-            po.big_count, big_cp, hp, L.s, v, offsets);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
-  HG_LAUNCH("hg_big_scan", k_big_scan, num_sms(), 1024, smBig, st, po.fine_start, po.big_list, po.big_count, L.s, v,
-            offsets);
+            po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
   HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, po.big_list,
-            po.big_count, big_cp, hp, L.s, v, offsets, edges);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
-  HG_LAUNCH("hg_big_fix", k_big_fix, num_sms(), 1024, smBig, st, po.fine_start, po.big_list, po.big_count, L.s, v,
-            offsets);
+            po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges);
   return HG_OK;
 }
 
@@ -1760,24 +1843,25 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   if (rc) return rc;
   if (split) HG_CHECK_CUDA(cudaEventRecord(split, st));  // query-side grouping done (intersect_timed's split)
   uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
-  const uint32_t max_items = (uint32_t)(L.nfine + q / kProbeChunk + 1);
-  uint32_t* item_bin = ws.take<uint32_t>(max_items);
+  const uint32_t max_extra = (uint32_t)(q / kProbeChunk + 1);
+  uint32_t* item_x = ws.take<uint32_t>(max_extra);
   uint32_t* big_bin = ws.take<uint32_t>(L.nfine + 1);
   uint32_t* big_t = ws.take<uint32_t>(L.nfine + 1);
   uint32_t* big_q = ws.take<uint32_t>(L.nfine + 1);
-  unsigned long long* plan = ws.take<unsigned long long>(kPlanWords);
+  unsigned long long* plan = reinterpret_cast<unsigned long long*>(po.plan32);
   const uint64_t hs = ht_slots(n_table, sizeof(K) * 8);
   K* hk = ws.take<K>(hs);
   uint32_t* hc = ws.take<uint32_t>(hs);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
-  HG_LAUNCH("hg_probe_plan", k_probe_plan, 1, 1024, 0, st, t_off, po.fine_start, L.nfine, L.s, v,
-            LocalShape<K>::kCap, item_bin, big_bin, big_t, big_q, plan);
+  HG_LAUNCH("hg_probe_plan", k_probe_plan, (L.nfine + 255) / 256, 256, 0, st, t_off, po.fine_start, L.nfine, L.s, v,
+            LocalShape<K>::kCap, item_x, big_bin, plan);
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
-  HG_LAUNCH("hg_local_probe", k_local_probe<H>, max_items, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
-            po.fine_start, item_bin, plan, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine + max_extra, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
+            po.fine_start, L.nfine, item_x, plan, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
   if (hs) {  // oversized table slices: key -> count hash table over the whole grid
-    HG_LAUNCH("hg_ht_clear", k_ht_clear<K>, num_sms() * 4, 256, 0, st, plan, hk, hc);
+    HG_LAUNCH("hg_ht_prep", k_ht_prep<K>, num_sms() * 4, 256, 0, st, plan, big_bin, t_off, po.fine_start, L.s, v, big_t,
+              big_q, hk, hc);
     HG_LAUNCH("hg_ht_insert", k_ht_insert<H>, num_sms() * 2, kHtT, 0, st, t_off, t_edges, L.s, v, big_bin, big_t, plan, hk,
               hc);
     HG_LAUNCH("hg_ht_lookup", k_ht_lookup<H>, num_sms() * 2, kHtT, 0, st, (const K*)po.grouped, po.fine_start, t_off, hp,
