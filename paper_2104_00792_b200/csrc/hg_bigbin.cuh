@@ -9,14 +9,19 @@
 // Such a bin must not serialise on one SM, so both sides work in chunks that
 // every CTA of the grid shares:
 //
-//   build   k_starts     lists the oversized bins, their chunk prefix
-//           k_local_build_p  zeroes their bucket counters (= the offsets slice)
-//           k_big_count  per chunk: smem counts, one global add per bucket;
-//                        the CTA finishing a bin's last chunk turns its
-//                        counts into bucket starts
-//           k_big_place  per chunk: smem ranks, one global claim per bucket,
-//                        keys stored at claim + rank; the CTA finishing a
-//                        bin's last chunk shifts the claimed ends to starts
+//   build   k_starts     lists the oversized bins: medium (<= kHugeBin keys)
+//                        and huge ones, the huge ones' chunk prefix
+//           k_local_build_p  zeroes the huge bins' bucket counters (= their
+//                        offsets slice)
+//           k_big_count  medium bin: one CTA counts, scans and places it
+//                        (smem counters, two passes over its keys);
+//                        huge-bin chunk: smem counts, one global add per
+//                        bucket; the CTA finishing a bin's last chunk turns
+//                        its counts into bucket starts
+//           k_big_place  huge-bin chunk: smem ranks, one global claim per
+//                        bucket, keys stored at claim + rank; the CTA
+//                        finishing a bin's last chunk shifts the claimed ends
+//                        to starts
 //   query   k_probe_plan per fine bin: extra probe work items for hot bins,
 //                        the list of bins whose table slice is oversized
 //           k_ht_prep    key -> count hash table for those bins (cleared),
@@ -35,11 +40,11 @@ struct BigShape {
 
 // Locate chunk k: bin index j, fine bin f, key range [lo, hi), chunks of j.
 __device__ __forceinline__ void big_chunk(uint32_t k, uint32_t nbig, uint32_t CH, const uint32_t* __restrict__ big_cp,
-                                          const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ fine_start,
+                                          const uint32_t* __restrict__ huge_list, const uint32_t* __restrict__ fine_start,
                                           uint32_t* s_loc) {
   if (threadIdx.x == 0) {
     const uint32_t j = upper_index(big_cp, nbig, k);
-    const uint32_t f = big_list[j];
+    const uint32_t f = *(huge_list - j);  // the huge list grows downwards
     const uint32_t lo = fine_start[f] + (k - big_cp[j]) * CH;
     s_loc[0] = f;
     s_loc[1] = lo;
@@ -72,22 +77,86 @@ __device__ __forceinline__ bool last_chunk(uint32_t* done, uint32_t j, uint32_t 
 // completes a bin's last chunk scans the counts into bucket starts.  `copy`
 // (two partition levels: the grouped keys sit in `edges`) also copies the
 // chunk to `dst` so placement can overwrite edges.
+// A medium oversized bin [lo, hi) (kCap < keys <= kHugeBin), whole, by one
+// CTA: smem counters for its 2^s buckets, a counting pass (lanes of a warp
+// that hit the same bucket share one atomic; `copy` also copies the keys to
+// `dst`), the scan into offsets, and a placing pass whose atomics return each
+// key's slot.
+template <typename H>
+__device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, KeyOf<H>* __restrict__ dst, int copy,
+                                           uint32_t lo, uint32_t hi, uint64_t first, const HashParams& hp, int s,
+                                           uint64_t v, uint32_t* cnt, uint32_t* __restrict__ offsets,
+                                           KeyOf<H>* __restrict__ edges) {
+  using K = KeyOf<H>;
+  const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  constexpr int U = 4;  // keys per thread per round, loads first
+  const uint32_t step = U * blockDim.x;
+  for (uint32_t r0 = lo; r0 < hi; r0 += step) {
+    K kv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      const bool ok = e < hi;
+      if (ok && copy) dst[e] = kv[u];
+      const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      if (ok && (peers & lt) == 0) atomicAdd(cnt + l, (uint32_t)__popc(peers));
+    }
+  }
+  __syncthreads();
+  block_exscan_rows(cnt, nb, lo);
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = cnt[i];
+  __syncthreads();
+  const K* from = copy ? dst : src;
+  for (uint32_t r0 = lo; r0 < hi; r0 += step) {
+    K kv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      kv[u] = e < hi ? from[e] : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const bool ok = r0 + u * blockDim.x + threadIdx.x < hi;
+      const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, l);
+      uint32_t b0 = 0;
+      if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
+      b0 = __shfl_sync(0xffffffffu, b0, __ffs(peers) - 1);
+      if (ok) edges[b0 + __popc(peers & lt)] = kv[u];
+    }
+  }
+  __syncthreads();
+}
+
 template <typename H>
 __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__ src, KeyOf<H>* __restrict__ dst, int copy,
                                                     const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
+                                                    const uint32_t* __restrict__ huge_list,
                                                     const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_cp,
                                                     uint32_t* __restrict__ done, HashParams hp, int s, uint64_t v,
-                                                    uint32_t* __restrict__ offsets) {
+                                                    uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
   __shared__ uint32_t s_loc[5];
-  const uint32_t nbig = *big_count;
-  if (nbig == 0) return;
-  const uint32_t nch = big_cp[nbig];
+  const uint32_t nmed = big_count[0], nbig = big_count[1];
+  const uint32_t nch = nbig ? big_cp[nbig] : 0u;
   const uint32_t lt = lanemask_lt();
+  for (uint32_t k = blockIdx.x; k < nmed; k += gridDim.x) {
+    const uint32_t f = big_list[k];
+    big_medium<H>(src, dst, copy, fine_start[f], fine_start[f + 1], (uint64_t)f << s, hp, s, v, cnt, offsets, edges);
+  }
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
-    big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
+    big_chunk(k, nbig, BS::kChunk, big_cp, huge_list, fine_start, s_loc);
     const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2], j = s_loc[3], nck = s_loc[4];
     const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
@@ -128,7 +197,7 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
 // bucket's start; the CTA that completed it shifts them back by one bucket.
 template <typename H>
 __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__ src, const uint32_t* __restrict__ fine_start,
-                                                    const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count,
+                                                    const uint32_t* __restrict__ huge_list, const uint32_t* __restrict__ big_count,
                                                     const uint32_t* __restrict__ big_cp, uint32_t* __restrict__ done,
                                                     HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets,
                                                     KeyOf<H>* __restrict__ edges) {
@@ -136,12 +205,12 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
   __shared__ uint32_t s_loc[5];
-  const uint32_t nbig = *big_count;
+  const uint32_t nbig = big_count[1];
   if (nbig == 0) return;
   const uint32_t nch = big_cp[nbig];
   const uint32_t lt = lanemask_lt();
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
-    big_chunk(k, nbig, BS::kChunk, big_cp, big_list, fine_start, s_loc);
+    big_chunk(k, nbig, BS::kChunk, big_cp, huge_list, fine_start, s_loc);
     const uint32_t f = s_loc[0], lo = s_loc[1], hi = s_loc[2], j = s_loc[3], nck = s_loc[4];
     const uint64_t first = (uint64_t)f << s;
     const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);

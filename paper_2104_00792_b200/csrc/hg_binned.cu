@@ -16,9 +16,13 @@
 //                       smem staging, one contiguous run per bin
 //   P2  k_part2         the same over each level-1 bin, claiming fine-bin space
 //   C   k_local_build   one CTA per fine bin: count, scan, place in smem,
-//                       write offsets + edges
-//   Q   k_local_probe   one CTA per fine bin: the table's CSR slice staged in
-//                       smem, the bin's queries probe it (IntersectArray)
+//                       write offsets + edges (bins above the smem capacity:
+//                       k_big_count / k_big_place, hg_bigbin.cuh)
+//   Q   k_local_probe   one CTA per fine bin (plus extra work items for hot
+//                       bins): the table's CSR slice staged in smem, deep
+//                       buckets sorted, the bin's queries probe it
+//                       (IntersectArray); slices above the smem capacity:
+//                       k_ht_* (hg_bigbin.cuh)
 //   R   k_unpart<2,1>   query answers back to input order: each tile's runs
 //                       are pulled into smem and read back through a u16 map
 //
@@ -340,10 +344,14 @@ __global__ void __launch_bounds__(1024) k_colscan(uint32_t* __restrict__ M, uint
 
 // One CTA: fine starts (F+1), level-1 starts (nb1+1), level-2 tile prefix
 // (nb1+1; tp[nb1] = level-2 tile count), fine cursors (= fine starts), the
-// list of fine bins above `cap` keys with its prefix of `big_chunk`-key chunks
-// (big_cp, nbig+1) and zeroed per-bin chunk-completion counters (big_done[j]
-// and big_done[nfine + 1 + j], j < nbig), and `nzero` zeroed words at `zero`
-// (the query's plan).
+// list of fine bins above `cap` keys (build only: big_list[0, big_count[0])
+// the medium ones, big_list[nfine - 1 - j], j < big_count[1], the ones above
+// kHugeBin keys) with the huge ones' prefix of `big_chunk`-key chunks (big_cp,
+// nhuge + 1) and zeroed per-bin chunk-completion counters (big_done[j] and
+// big_done[nfine + 1 + j]), and `nzero` zeroed words at `zero` (the query's
+// plan).
+constexpr uint32_t kHugeBin = 1u << 16;  // oversized bins above this are built by many CTAs in chunks
+
 __global__ void __launch_bounds__(1024)
 k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, uint32_t nb1, uint32_t tile,
          uint32_t cap, uint32_t* __restrict__ fine_start, uint32_t* __restrict__ c_start, uint32_t* __restrict__ tp,
@@ -352,14 +360,17 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
          uint32_t nzero) {
   for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0;
   extern __shared__ uint32_t s_a[];  // nfine + nb1 + 1
-  __shared__ uint32_t s_big;
+  __shared__ uint32_t s_big, s_huge;
   uint32_t* s_t = s_a + nfine;
-  if (threadIdx.x == 0) s_big = 0;
+  if (threadIdx.x == 0) s_big = s_huge = 0;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
     const uint32_t t = fine_cnt[i];
     s_a[i] = t;
-    if (t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
+    // oversized bins: medium ones from the front of the list, huge ones
+    // (> kHugeBin keys, built in chunks by many CTAs) from the back
+    if (t > kHugeBin && big_cp) big_list[nfine - 1 - atomicAdd(&s_huge, 1u)] = i;
+    else if (t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
   }
   __syncthreads();
   const uint32_t total = block_exscan_rows(s_a, nfine, 0);  // warp-row layout: no bank conflicts
@@ -369,7 +380,8 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
   }
   if (threadIdx.x == 0) {
     fine_start[nfine] = total;
-    *big_count = s_big;
+    big_count[0] = s_big;
+    big_count[1] = s_huge;
   }
   for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) {
     const uint32_t a = s_a[c * group];
@@ -383,14 +395,14 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
   for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) tp[c] = s_t[c];
   if (threadIdx.x == 0) tp[nb1] = ntiles;
   // oversized bins (hg_bigbin.cuh): chunk prefix, completion counters
-  const uint32_t nbig = s_big;
+  const uint32_t nbig = s_huge;
   if (big_cp == nullptr || nbig == 0) return;
   uint32_t carry = 0;
   for (uint32_t base = 0; base < nbig; base += blockDim.x) {
     const uint32_t j = base + threadIdx.x;
     uint32_t c = 0;
     if (j < nbig) {
-      const uint32_t f = big_list[j];
+      const uint32_t f = big_list[nfine - 1 - j];
       const uint32_t hi = f + 1 < nfine ? s_a[f + 1] : total;
       c = (hi - s_a[f] + big_chunk - 1) / big_chunk;
     }
@@ -1000,13 +1012,16 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
   K* raw = reinterpret_cast<K*>(s_raw + PS::c16_bytes(s));            // next bin's keys (TMA)
   K* staged = raw + PS::kElems;                                       // this bin's edges, chunk-aligned to global
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets[v] = fine_start[nfine];
-  // bins above kCap belong to k_big_count / k_big_place; their bucket
-  // counters (the offsets slice) are zeroed here
+  // bins above kCap belong to k_big_count / k_big_place; the bucket counters
+  // (the offsets slice) of those above kHugeBin are zeroed here
   auto next_small = [&](uint32_t f) -> uint32_t {
-    while (f < nfine && fine_start[f + 1] - fine_start[f] > kCap) {
-      const uint64_t fb = (uint64_t)f << s;
-      const uint32_t nbz = (uint32_t)min((uint64_t)S, v - fb);
-      for (uint32_t l = threadIdx.x; l < nbz; l += NT) offsets[fb + l] = 0;
+    uint32_t sz;
+    while (f < nfine && (sz = fine_start[f + 1] - fine_start[f]) > kCap) {
+      if (sz > kHugeBin) {
+        const uint64_t fb = (uint64_t)f << s;
+        const uint32_t nbz = (uint32_t)min((uint64_t)S, v - fb);
+        for (uint32_t l = threadIdx.x; l < nbz; l += NT) offsets[fb + l] = 0;
+      }
       f += gridDim.x;
     }
     return f;
@@ -1148,75 +1163,8 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
   if (threadIdx.x == 0) tma_store_wait_all();
 }
 
-// Fine bins above the smem capacity (high-duplicate inputs): the bin's keys
-// stream from global memory twice while the 2^s counters stay in smem.  Lanes
-// of a warp that hit the same bucket (the common case here: few distinct keys,
-// thousands of copies each) share one atomic (match_any), and the rank of each
-// lane inside its group comes from the group mask.  When `copy` is set the
-// count pass also copies the bin from `edges` into `src` (same offsets) so
-// placement can overwrite edges.
-template <typename H>
-__global__ void __launch_bounds__(1024)
-k_local_build_big(KeyOf<H>* src, int copy, const uint32_t* __restrict__ fine_start, const uint32_t* __restrict__ big_list,
-                  const uint32_t* __restrict__ big_count, HashParams hp, int s, uint64_t v, uint32_t* __restrict__ scratch,
-                  uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
-  using K = typename H::Key;
-  (void)scratch;
-  extern __shared__ uint32_t cnt[];  // 2^s counters
-  const uint32_t S = 1u << s;
-  const uint32_t lt = lanemask_lt();
-  for (uint32_t k = blockIdx.x; k < *big_count; k += gridDim.x) {
-    const uint32_t f = big_list[k];
-    const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
-    const uint64_t first = (uint64_t)f << s;
-    const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    // U keys per thread per round, loads first (the loop is latency-bound otherwise)
-    constexpr int U = 4;
-    const uint32_t step = U * blockDim.x;
-    for (uint32_t r0 = lo; r0 < hi; r0 += step) {
-      K kv[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
-        kv[u] = j < hi ? (copy ? edges[j] : src[j]) : K(0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
-        const bool ok = j < hi;
-        if (ok && copy) src[j] = kv[u];
-        const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, l);
-        if (ok && (peers & lt) == 0) atomicAdd(cnt + l, (uint32_t)__popc(peers));
-      }
-    }
-    __syncthreads();
-    block_exscan_rows(cnt, nb, lo);
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = cnt[i];
-    __syncthreads();
-    for (uint32_t r0 = lo; r0 < hi; r0 += step) {
-      K kv[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const uint32_t j = r0 + u * blockDim.x + threadIdx.x;
-        kv[u] = j < hi ? src[j] : K(0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const bool ok = r0 + u * blockDim.x + threadIdx.x < hi;
-        const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, l);
-        uint32_t b0 = 0;
-        if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
-        b0 = __shfl_sync(0xffffffffu, b0, __ffs(peers) - 1);
-        if (ok) edges[b0 + __popc(peers & lt)] = kv[u];
-      }
-    }
-    __syncthreads();
-  }
-}
+// Fine bins above the smem capacity (high-duplicate inputs) are built by
+// k_big_count / k_big_place (hg_bigbin.cuh).
 
 // --------------------------------------------------------------------------- Q: probe
 
@@ -1825,10 +1773,11 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   const int copy = L.two_level ? 1 : 0;
   const size_t smBig = (size_t)(1u << L.s) * 4;
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_count<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  const uint32_t* huge_list = po.big_list + L.nfine - 1;  // grows downwards (k_starts)
   HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, src, copy, po.fine_start, po.big_list,
-            po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets);
+            huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
-  HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, po.big_list,
+  HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, huge_list,
             po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges);
   return HG_OK;
 }
