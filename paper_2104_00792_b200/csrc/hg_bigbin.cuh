@@ -92,7 +92,7 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
   const uint32_t lt = lanemask_lt();
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
-  constexpr int U = 4;  // keys per thread per round, loads first
+  constexpr int U = BigShape<K>::kKPT;  // keys per thread per round (a bin of <= kChunk keys: one round)
   const uint32_t step = U * blockDim.x;
   for (uint32_t r0 = lo; r0 < hi; r0 += step) {
     K kv[U];

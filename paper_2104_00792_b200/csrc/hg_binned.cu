@@ -1291,6 +1291,40 @@ __device__ __noinline__ uint32_t map_count(const BigMap<K>& m, K key) {
 // is valid, so no bounds checks; bin_flags -- which depth classes the bin has
 // (known from staging): only then are queries checked for the sorted search
 // or the map.
+// Count of q in the sorted bucket te[a, a + d) for lanes with `srt` (others
+// keep c): lower and upper bound in one warp-uniform loop of
+// floor(log2(max d)) + 1 steps (two independent search chains).  Warp-
+// collective; out of line so the probe's unrolled batch loop stays small
+// enough for the instruction cache.
+template <typename K>
+__device__ __noinline__ uint32_t sorted_count(const K* te, uint32_t a, uint32_t d, K q, bool srt, uint32_t c) {
+  const uint32_t smax = __reduce_max_sync(0xffffffffu, srt ? d : 0u);
+  if (!smax) return c;
+  uint32_t lb = a, ln = srt ? d : 0u, ub = a, un = ln;
+  const int steps = 32 - __clz(smax);
+  for (int it = 0; it < steps; it++) {
+    const uint32_t hl = ln >> 1, hu = un >> 1;
+    const K xl = te[lb + hl], xu = te[ub + hu];
+    if (ln) {
+      if (xl < q) {
+        lb += hl + 1;
+        ln -= hl + 1;
+      } else {
+        ln = hl;
+      }
+    }
+    if (un) {
+      if (!(q < xu)) {
+        ub += hu + 1;
+        un -= hu + 1;
+      } else {
+        un = hu;
+      }
+    }
+  }
+  return srt ? ub - lb : c;
+}
+
 template <typename H, bool kFull>
 __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const HashParams& hp, uint32_t first,
                                             const uint16_t* off16, const KeyOf<H>* te, const BigMap<KeyOf<H>>& map,
@@ -1332,36 +1366,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
     }
-    if (bin_flags & kBinSort) {
-      // sorted bucket: lower and upper bound in one warp-uniform loop of
-      // floor(log2(max d)) + 1 steps (two independent search chains)
-      const uint32_t smax = __reduce_max_sync(0xffffffffu, srt ? d : 0u);
-      if (smax) {
-        uint32_t lb = a, ln = srt ? d : 0u, ub = a, un = ln;
-        const int steps = 32 - __clz(smax);
-        for (int it = 0; it < steps; it++) {
-          const uint32_t hl = ln >> 1, hu = un >> 1;
-          const K xl = te[lb + hl], xu = te[ub + hu];
-          if (ln) {
-            if (xl < q) {
-              lb += hl + 1;
-              ln -= hl + 1;
-            } else {
-              ln = hl;
-            }
-          }
-          if (un) {
-            if (!(q < xu)) {
-              ub += hu + 1;
-              un -= hu + 1;
-            } else {
-              un = hu;
-            }
-          }
-        }
-        if (srt) c = ub - lb;
-      }
-    }
+    if (bin_flags & kBinSort) c = sorted_count<K>(te, a, d, q, srt, c);
     if (use_map && mapped) c = map_count(map, q);
     const uint32_t j = q0 + k * kT + threadIdx.x;
     if (kFull || j < qhi) {
