@@ -260,10 +260,12 @@ enum : int { kPlanItems = 0, kPlanBig, kPlanBigT, kPlanBigQ, kPlanCap, kPlanOnes
 constexpr uint32_t kProbeChunk = 32768;  // queries per shared-memory probe work item
 
 // One thread per fine bin f with queries (tn table keys, qn queries).  A bin
-// whose table slice fits smem is probed by CTA f (its first kProbeChunk
-// queries) plus one extra work item per further chunk (item = f | c << 15);
-// a larger slice goes to the hash-table path (big_bin list).  List order is
-// free: every consumer works from the lists as written.
+// whose table slice fits smem (or a medium slice, <= 4 kCap keys: the slice
+// map) is probed by CTA f (its first kProbeChunk queries) plus one extra work
+// item per further chunk (item = f | c << 15); a larger slice goes to the
+// hash-table path (big_bin list; k_local_probe adds medium slices with too
+// many distinct keys).  List order is free: every consumer works from the
+// lists as written.
 __global__ void k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t* __restrict__ q_start, uint32_t nfine,
                              int s, uint64_t v, uint32_t cap, uint32_t* __restrict__ item_x, uint32_t* __restrict__ big_bin,
                              unsigned long long* __restrict__ plan) {
@@ -272,7 +274,7 @@ __global__ void k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t*
   const uint32_t qn = q_start[f + 1] - q_start[f];
   if (qn == 0) return;
   const uint32_t tn = t_off[min((uint64_t)(f + 1) << s, v)] - t_off[(uint64_t)f << s];
-  if (tn > cap) {
+  if (tn > 4 * cap) {  // above kMapSlice = 4 kCap: the slice is too long to stream per work item
     big_bin[atomicAdd(plan + kPlanBig, 1ull)] = f;
     atomicAdd(plan + kPlanBigT, (unsigned long long)tn);
     atomicAdd(plan + kPlanBigQ, (unsigned long long)qn);
@@ -283,9 +285,154 @@ __global__ void k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t*
   }
 }
 
+// slot hash of the key -> count tables (independent of the bucket hash)
+__device__ __forceinline__ uint64_t ht_slot_mix(uint64_t key) {
+  return fmix64(key * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull);
+}
+
+__device__ __forceinline__ uint32_t cas_key(uint32_t* p, uint32_t cmp, uint32_t val) { return atomicCAS(p, cmp, val); }
+__device__ __forceinline__ uint64_t cas_key(uint64_t* p, uint64_t cmp, uint64_t val) {
+  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp, (unsigned long long)val);
+}
+
+// ---- medium table slices (kCap < keys <= kMapSlice): the probe CTA cannot
+// stage the slice, but high-duplicate slices (few distinct keys, e.g. C3) fit
+// a key -> count map in shared memory, built by streaming the slice (its
+// equal keys are adjacent: a bucket's keys are contiguous in the CSR) and
+// answering every query with one lookup.  A slice with more distinct keys
+// than half the map goes to the global hash table instead.
+template <typename K>
+struct SliceMapShape {
+  static constexpr uint32_t kSlots = sizeof(K) == 4 ? 8192 : 4096;  // fits the probe's smem at any s
+};
+
+template <typename K>
+__device__ __forceinline__ uint32_t smap_slot(K key) {
+  return (uint32_t)ht_slot_mix((uint64_t)key);
+}
+
+// Add `add` occurrences of key (all-ones key counted in *ones); false when the
+// map is full (the caller flags overflow).
+template <typename K>
+__device__ __forceinline__ bool smap_add(K* mk, uint32_t* mc, uint32_t* claimed, uint32_t* ones, K key, uint32_t add) {
+  constexpr uint32_t M = SliceMapShape<K>::kSlots;
+  if (key == ~K(0)) {
+    atomicAdd(ones, add);
+    return true;
+  }
+  uint32_t i = smap_slot(key) & (M - 1);
+  for (uint32_t probe = 0; probe < M; probe++, i = (i + 1) & (M - 1)) {
+    K cur = mk[i];
+    if (cur == ~K(0)) {
+      cur = cas_key(mk + i, ~K(0), key);
+      if (cur == ~K(0)) {
+        atomicAdd(claimed, 1u);
+        cur = key;
+      }
+    }
+    if (cur == key) {
+      atomicAdd(mc + i, add);
+      return true;
+    }
+  }
+  return false;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t smap_count(const K* mk, const uint32_t* mc, uint32_t ones, K key) {
+  constexpr uint32_t M = SliceMapShape<K>::kSlots;
+  if (key == ~K(0)) return ones;
+  uint32_t i = smap_slot(key) & (M - 1);
+  for (uint32_t probe = 0; probe < M; probe++, i = (i + 1) & (M - 1)) {
+    const K cur = mk[i];
+    if (cur == key) return mc[i];
+    if (cur == ~K(0)) return 0;
+  }
+  return 0;
+}
+
+// The probe of one work item over a medium slice [tlo, thi) of fine bin f.
+// Returns false (nothing written) when the slice has too many distinct keys;
+// the first chunk's CTA then hands the bin to the hash-table path.
+template <typename H>
+__device__ __noinline__ bool probe_slice_map(const KeyOf<H>* __restrict__ t_edges, const uint32_t* __restrict__ t_off,
+                                             uint32_t tlo, uint32_t thi, const KeyOf<H>* __restrict__ qpart,
+                                             uint32_t qlo, uint32_t qhi, const HashParams& hp, unsigned char* smem,
+                                             uint32_t* __restrict__ mult_bo, unsigned long long* __restrict__ agg) {
+  using K = KeyOf<H>;
+  constexpr uint32_t M = SliceMapShape<K>::kSlots;
+  K* mk = reinterpret_cast<K*>(smem);
+  uint32_t* mc = reinterpret_cast<uint32_t*>(smem + M * sizeof(K));
+  __shared__ uint32_t s_claimed, s_ones, s_full;
+  for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
+    mk[i] = ~K(0);
+    mc[i] = 0;
+  }
+  if (threadIdx.x == 0) s_claimed = s_ones = s_full = 0;
+  __syncthreads();
+  // warp w streams a contiguous range of 32-key rows, 8 rows in flight; each
+  // lane counts runs of equal keys and adds a run when its key changes
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t tn = thi - tlo;
+  const uint32_t rows = (tn + 31) / 32;
+  const uint32_t per = (rows + nw - 1) / nw;
+  const uint32_t r0 = warp * per, r1 = min(rows, r0 + per);
+  K cur = K(0);
+  uint32_t run = 0;
+  bool ok = true;
+  for (uint32_t r = r0; r < r1; r += 8) {
+    K kv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t t = (r + u) * 32 + lane;
+      kv[u] = (r + u < r1 && t < tn) ? __ldcs(t_edges + tlo + t) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t t = (r + u) * 32 + lane;
+      if (r + u < r1 && t < tn) {
+        if (run && kv[u] != cur) {
+          ok &= smap_add(mk, mc, &s_claimed, &s_ones, cur, run);
+          run = 0;
+        }
+        cur = kv[u];
+        run++;
+      }
+    }
+  }
+  if (run) ok &= smap_add(mk, mc, &s_claimed, &s_ones, cur, run);
+  if (!ok) s_full = 1;
+  __syncthreads();
+  if (s_full || s_claimed > M / 2) return false;
+  const uint32_t ones = s_ones;
+  uint64_t matched = 0, total = 0, comps = 0;
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += 4 * blockDim.x) {
+    K qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t j = q0 + u * blockDim.x + threadIdx.x;
+      qv[u] = j < qhi ? __ldcs(qpart + j) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t j = q0 + u * blockDim.x + threadIdx.x;
+      if (j < qhi) {
+        const uint32_t h = H::bucket(qv[u], hp);
+        const uint32_t c = smap_count(mk, mc, ones, qv[u]);
+        mult_bo[j] = c;
+        matched += c != 0;
+        total += c;
+        comps += t_off[(uint64_t)h + 1] - t_off[h];
+      }
+    }
+  }
+  if (agg) flush_agg(matched, total, comps, agg);
+  return true;
+}
+
 template <typename K>
 __device__ __forceinline__ uint64_t ht_slot(K key) {
-  return fmix64((uint64_t)key * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull);
+  return ht_slot_mix((uint64_t)key);
 }
 
 __device__ __forceinline__ unsigned long long ht_capacity(unsigned long long keys) {
@@ -334,11 +481,6 @@ __global__ void k_ht_prep(unsigned long long* __restrict__ plan, const uint32_t*
     big_t[nbig] = ct;
     big_q[nbig] = cq;
   }
-}
-
-__device__ __forceinline__ uint32_t cas_key(uint32_t* p, uint32_t cmp, uint32_t val) { return atomicCAS(p, cmp, val); }
-__device__ __forceinline__ uint64_t cas_key(uint64_t* p, uint64_t cmp, uint64_t val) {
-  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp, (unsigned long long)val);
 }
 
 // Add `add` occurrences of `key`.  The all-ones key is the empty marker and is

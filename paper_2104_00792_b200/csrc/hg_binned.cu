@@ -1466,7 +1466,7 @@ template <typename H>
 __global__ void __launch_bounds__(kT, 2)
 k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t_edges, const KeyOf<H>* __restrict__ qpart,
               const uint32_t* __restrict__ q_start, uint32_t nfine, const uint32_t* __restrict__ item_x,
-              const unsigned long long* __restrict__ plan, HashParams hp, int s, uint64_t v,
+              unsigned long long* __restrict__ plan, uint32_t* __restrict__ big_bin, HashParams hp, int s, uint64_t v,
               uint32_t* __restrict__ mult_bo, unsigned long long* __restrict__ agg) {
   using K = typename H::Key;
   constexpr uint32_t VPL = 16 / sizeof(K);
@@ -1495,7 +1495,15 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
   const uint32_t tn = thi - tlo;
-  if (tn > kCap) return;  // the hash-table path answers this bin (k_ht_lookup)
+  if (tn > kCap) {  // medium slice: key -> count map; else (or too many distinct keys) the hash-table path
+    if (tn <= 4 * kCap && probe_slice_map<H>(t_edges, t_off, tlo, thi, qpart, qlo, qhi, hp, s_raw, mult_bo, agg)) return;
+    if (tn <= 4 * kCap && c == 0 && threadIdx.x == 0) {  // k_probe_plan left it to the probe: hand it over
+      big_bin[atomicAdd(plan + kPlanBig, 1ull)] = f;
+      atomicAdd(plan + kPlanBigT, (unsigned long long)tn);
+      atomicAdd(plan + kPlanBigQ, (unsigned long long)(q_start[f + 1] - q_start[f]));
+    }
+    return;
+  }
   // edges: one TMA bulk copy of the 16-byte chunks from the boundary below
   // tlo (tedges[sh + j] = edge tlo + j) lands while the offsets convert
   const uint32_t a0 = tlo & ~(VPL - 1);
@@ -1812,7 +1820,7 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
   HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine + max_extra, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
-            po.fine_start, L.nfine, item_x, plan, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
+            po.fine_start, L.nfine, item_x, plan, big_bin, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
   if (hs) {  // oversized table slices: key -> count hash table over the whole grid
     HG_LAUNCH("hg_ht_prep", k_ht_prep<K>, num_sms() * 4, 256, 0, st, plan, big_bin, t_off, po.fine_start, L.s, v, big_t,
               big_q, hk, hc);
