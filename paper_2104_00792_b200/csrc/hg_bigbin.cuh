@@ -311,8 +311,9 @@ __device__ __forceinline__ uint32_t smap_slot(K key) {
   return (uint32_t)ht_slot_mix((uint64_t)key);
 }
 
-// Add `add` occurrences of key (all-ones key counted in *ones); false when the
-// map is full (the caller flags overflow).
+// Add `add` occurrences of key (all-ones key counted in *ones); false once the
+// map holds more than M / 2 distinct keys or a probe sequence runs long (the
+// caller flags overflow and stops streaming).
 template <typename K>
 __device__ __forceinline__ bool smap_add(K* mk, uint32_t* mc, uint32_t* claimed, uint32_t* ones, K key, uint32_t add) {
   constexpr uint32_t M = SliceMapShape<K>::kSlots;
@@ -320,8 +321,9 @@ __device__ __forceinline__ bool smap_add(K* mk, uint32_t* mc, uint32_t* claimed,
     atomicAdd(ones, add);
     return true;
   }
+  if (*(volatile uint32_t*)claimed > M / 2) return false;  // too many distinct keys: give up early
   uint32_t i = smap_slot(key) & (M - 1);
-  for (uint32_t probe = 0; probe < M; probe++, i = (i + 1) & (M - 1)) {
+  for (uint32_t probe = 0; probe < 256; probe++, i = (i + 1) & (M - 1)) {
     K cur = mk[i];
     if (cur == ~K(0)) {
       cur = cas_key(mk + i, ~K(0), key);
@@ -380,7 +382,7 @@ __device__ __noinline__ bool probe_slice_map(const KeyOf<H>* __restrict__ t_edge
   K cur = K(0);
   uint32_t run = 0;
   bool ok = true;
-  for (uint32_t r = r0; r < r1; r += 8) {
+  for (uint32_t r = r0; r < r1 && __all_sync(0xffffffffu, ok); r += 8) {
     K kv[8];
 #pragma unroll
     for (int u = 0; u < 8; u++) {

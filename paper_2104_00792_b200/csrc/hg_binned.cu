@@ -1344,19 +1344,27 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
     }
   }
-  bool deep = false;
+  bool deep = false, sortq = false;
   if (bin_flags & kBinMap) {
 #pragma unroll
     for (int k = 0; k < QPT; k++) deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
   }
+  if (bin_flags & kBinSort) {
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      const uint32_t d = (ae[k] >> 16) - (ae[k] & 0xFFFFu);
+      sortq |= d > kLinDeg && d <= kSortMax;
+    }
+  }
   const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
+  const bool use_sort = __any_sync(0xffffffffu, sortq);  // some query of this warp's batch needs the sorted search
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
     if (!kFull && (uint32_t)k >= kmax) break;
     const K q = qv[k];
     const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
     const bool mapped = use_map && d > kBigDeg;
-    const bool srt = (bin_flags & kBinSort) && d > kLinDeg && d <= kSortMax;
+    const bool srt = use_sort && d > kLinDeg && d <= kSortMax;
     const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
     uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
                  (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
@@ -1366,7 +1374,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
     }
-    if (bin_flags & kBinSort) c = sorted_count<K>(te, a, d, q, srt, c);
+    if (use_sort) c = sorted_count<K>(te, a, d, q, srt, c);
     if (use_map && mapped) c = map_count(map, q);
     const uint32_t j = q0 + k * kT + threadIdx.x;
     if (kFull || j < qhi) {
