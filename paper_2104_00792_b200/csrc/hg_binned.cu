@@ -1291,18 +1291,15 @@ __device__ __noinline__ uint32_t map_count(const BigMap<K>& m, K key) {
 // is valid, so no bounds checks; bin_flags -- which depth classes the bin has
 // (known from staging): only then are queries checked for the sorted search
 // or the map.
-// Count of q in the sorted bucket te[a, a + d) for lanes with `srt` (others
-// keep c): lower and upper bound in one warp-uniform loop of
-// floor(log2(max d)) + 1 steps (two independent search chains).  Warp-
-// collective; out of line so the probe's unrolled batch loop stays small
+// Count of q in the sorted bucket te[a, a + d): lower and upper bound by
+// binary search (two independent chains, floor(log2 d) + 1 steps).  Per lane
+// and out of line, like map_count: only the few lanes whose bucket is in the
+// sorted class pay for it, and the probe's unrolled batch loop stays small
 // enough for the instruction cache.
 template <typename K>
-__device__ __noinline__ uint32_t sorted_count(const K* te, uint32_t a, uint32_t d, K q, bool srt, uint32_t c) {
-  const uint32_t smax = __reduce_max_sync(0xffffffffu, srt ? d : 0u);
-  if (!smax) return c;
-  uint32_t lb = a, ln = srt ? d : 0u, ub = a, un = ln;
-  const int steps = 32 - __clz(smax);
-  for (int it = 0; it < steps; it++) {
+__device__ __noinline__ uint32_t sorted_count(const K* te, uint32_t a, uint32_t d, K q) {
+  uint32_t lb = a, ln = d, ub = a, un = d;
+  while (ln | un) {
     const uint32_t hl = ln >> 1, hu = un >> 1;
     const K xl = te[lb + hl], xu = te[ub + hu];
     if (ln) {
@@ -1322,7 +1319,7 @@ __device__ __noinline__ uint32_t sorted_count(const K* te, uint32_t a, uint32_t 
       }
     }
   }
-  return srt ? ub - lb : c;
+  return ub - lb;
 }
 
 template <typename H, bool kFull>
@@ -1344,27 +1341,19 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
     }
   }
-  bool deep = false, sortq = false;
+  bool deep = false;
   if (bin_flags & kBinMap) {
 #pragma unroll
     for (int k = 0; k < QPT; k++) deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
   }
-  if (bin_flags & kBinSort) {
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t d = (ae[k] >> 16) - (ae[k] & 0xFFFFu);
-      sortq |= d > kLinDeg && d <= kSortMax;
-    }
-  }
   const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
-  const bool use_sort = __any_sync(0xffffffffu, sortq);  // some query of this warp's batch needs the sorted search
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
     if (!kFull && (uint32_t)k >= kmax) break;
     const K q = qv[k];
     const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
     const bool mapped = use_map && d > kBigDeg;
-    const bool srt = use_sort && d > kLinDeg && d <= kSortMax;
+    const bool srt = (bin_flags & kBinSort) && d > kLinDeg && d <= kSortMax;
     const K e0 = te[a], e1 = te[a + 1], e2 = te[a + 2], e3 = te[a + 3];
     uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
                  (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
@@ -1374,7 +1363,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
     }
-    if (use_sort) c = sorted_count<K>(te, a, d, q, srt, c);
+    if (srt) c = sorted_count<K>(te, a, d, q);
     if (use_map && mapped) c = map_count(map, q);
     const uint32_t j = q0 + k * kT + threadIdx.x;
     if (kFull || j < qhi) {
