@@ -1183,12 +1183,25 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
 }
 
 #ifndef HG_PROBE_QPT
-#define HG_PROBE_QPT 8
+#define HG_PROBE_QPT 4
 #endif
-constexpr int kProbeQPT = HG_PROBE_QPT;  // queries per thread per probe batch (the next batch is prefetched)
+#ifndef HG_PROBE_QPT64
+#define HG_PROBE_QPT64 8
+#endif
+#ifndef HG_PROBE_NOFULL
+#define HG_PROBE_NOFULL 0  // experiment: one batch variant (bounds-checked) instead of two
+#endif
+// queries per thread per probe batch (the next batch is prefetched); 64-bit
+// keys use fewer: their unrolled batch loop otherwise overflows the
+// instruction cache and the register file
+template <typename K>
+struct ProbeQ {
+  static constexpr int kQPT = sizeof(K) == 4 ? HG_PROBE_QPT : HG_PROBE_QPT64;
+};
 
 template <typename K>
-__device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qhi, K (&qv)[kProbeQPT]) {
+__device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qhi, K (&qv)[ProbeQ<K>::kQPT]) {
+  constexpr int kProbeQPT = ProbeQ<K>::kQPT;
 #pragma unroll
   for (int k = 0; k < kProbeQPT; k++) {
     const uint32_t j = q0 + k * kT + threadIdx.x;
@@ -1326,10 +1339,10 @@ template <typename H, bool kFull>
 __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const HashParams& hp, uint32_t first,
                                             const uint16_t* off16, const KeyOf<H>* te, const BigMap<KeyOf<H>>& map,
                                             bool overflow, uint32_t bin_flags, uint32_t* __restrict__ mult_bo,
-                                            const KeyOf<H> (&qv)[kProbeQPT], uint32_t& m32, uint32_t& t32,
+                                            const KeyOf<H> (&qv)[ProbeQ<KeyOf<H>>::kQPT], uint32_t& m32, uint32_t& t32,
                                             uint32_t& d32) {
   using K = typename H::Key;
-  constexpr int QPT = kProbeQPT;
+  constexpr int QPT = ProbeQ<K>::kQPT;
   const uint32_t kmax = kFull ? (uint32_t)QPT : (qhi - q0 + kT - 1) / kT;  // query slots this batch fills
   uint32_t ae[QPT];
 #pragma unroll
@@ -1347,6 +1360,10 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
     for (int k = 0; k < QPT; k++) deep |= (ae[k] >> 16) - (ae[k] & 0xFFFFu) > kBigDeg;
   }
   const bool use_map = __any_sync(0xffffffffu, deep) && !overflow;
+  // slots answered after the batch by the sorted search or the map (one call
+  // site each, outside the unrolled loop: the loop stays small enough for the
+  // instruction cache and no registers are saved around calls inside it)
+  uint32_t rare = 0;
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
     if (!kFull && (uint32_t)k >= kmax) break;
@@ -1363,15 +1380,34 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
     }
-    if (srt) c = sorted_count<K>(te, a, d, q);
-    if (use_map && mapped) c = map_count(map, q);
     const uint32_t j = q0 + k * kT + threadIdx.x;
     if (kFull || j < qhi) {
-      mult_bo[j] = c;
-      m32 += (c != 0);
-      t32 += c;
       d32 += d;
+      if (mapped || srt) {
+        rare |= 1u << k;
+      } else {
+        mult_bo[j] = c;
+        m32 += (c != 0);
+        t32 += c;
+      }
     }
+  }
+  while (rare) {
+    const int k = __ffs(rare) - 1;
+    rare &= rare - 1;
+    K q = qv[0];
+    uint32_t e = ae[0];
+#pragma unroll
+    for (int i = 1; i < QPT; i++)
+      if (i == k) {
+        q = qv[i];
+        e = ae[i];
+      }
+    const uint32_t a = e & 0xFFFFu, d = (e >> 16) - a;
+    const uint32_t c = d > kBigDeg ? map_count(map, q) : sorted_count<K>(te, a, d, q);
+    mult_bo[q0 + k * kT + threadIdx.x] = c;
+    m32 += (c != 0);
+    t32 += c;
   }
 }
 
@@ -1380,10 +1416,10 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
                                                    const HashParams& hp, uint32_t first, const uint16_t* off16,
                                                    const KeyOf<H>* te, const BigMap<KeyOf<H>>& map, bool overflow,
                                                    uint32_t bin_flags, uint32_t* __restrict__ mult_bo,
-                                                   KeyOf<H> (&qv)[kProbeQPT], uint64_t& matched, uint64_t& total,
+                                                   KeyOf<H> (&qv)[ProbeQ<KeyOf<H>>::kQPT], uint64_t& matched, uint64_t& total,
                                                    uint64_t& comps) {
   using K = typename H::Key;
-  constexpr int QPT = kProbeQPT;
+  constexpr int QPT = ProbeQ<K>::kQPT;
   constexpr uint32_t B = QPT * kT;
   K qn[QPT];  // the next batch, in flight while this one is probed
   for (uint32_t q0 = qlo; q0 < qhi; q0 += B) {
@@ -1393,7 +1429,7 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
     }
     if (q0 + B < qhi) load_queries<K>(qpart, q0 + B, qhi, qn);
     uint32_t m32 = 0, t32 = 0, d32 = 0;
-    if (qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
+    if (!HG_PROBE_NOFULL && qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
     else probe_batch<H, false>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
     matched += m32;
     total += t32;
@@ -1486,7 +1522,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const uint32_t qlo = q_start[f] + c * kProbeChunk;
   uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
   if (qlo >= qhi) return;
-  K qv[kProbeQPT];
+  K qv[ProbeQ<K>::kQPT];
   load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
@@ -1620,7 +1656,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   const bool overflow = map.full != 0;
   uint64_t matched = 0, total = 0, comps = 0;
 #if defined(HG_EXP_PROBE) && HG_EXP_PROBE == 3  // timing experiment (tools/build_variant.py): first batch only
-  qhi = min(qhi, qlo + kProbeQPT * kT);
+  qhi = min(qhi, qlo + ProbeQ<K>::kQPT * kT);
 #endif
   probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, bin_flags, mult_bo, qv, matched,
                         total, comps);
