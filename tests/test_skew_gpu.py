@@ -158,3 +158,83 @@ def test_sorted_bucket_depth_boundaries():
     mult, matched, total, comp, _ = O.query(off, placed, queries, kind=O.KIND_IDENTITY)
     assert np.array_equal(res.multiplicities, mult)
     assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
+
+
+# --------------------------------------------------------------------------- timed robustness (device time)
+
+
+def _device_ms(fn, reps=3):
+    import torch
+
+    ts = []
+    for _ in range(reps + 1):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        out = fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return sorted(ts[1:])[reps // 2], out
+
+
+def _device_keys(kind, n, seed):
+    import torch
+
+    if kind == "uniform":
+        return hg.generate_device(hg.WorkloadSpec(hg.WorkloadKind.RANDOM_WITH_REPLACEMENT, 26, n, seed))
+    if kind == "identical":
+        return torch.full((n,), 7, dtype=torch.int32, device="cuda")
+    keys = zipf_keys(n, seed, 1.1)
+    return torch.from_numpy(keys.view(np.int32)).cuda()
+
+
+def test_c05_build_throughput_flat_across_duplicate_rates():
+    """acceptance c05 on the GPU (test_acceptance.py:166-178): build throughput
+    within 2x across duplicate rates 1..128, at 2^26 keys."""
+    n = 1 << 26
+    keys = _device_keys("uniform", n, 0)
+    rates = []
+    for d in (1, 2, 4, 8, 16, 32, 64, 128):
+        ms, _ = _device_ms(lambda: hg.build(keys, 1.0, hash_range=n // d))
+        rates.append(n / ms)
+    assert max(rates) / min(rates) <= 2.0, rates
+
+
+@pytest.mark.parametrize("kind", ["identical", "zipf"])
+def test_skewed_inputs_within_bounds_of_uniform(kind):
+    """A hot key must not serialise on one SM: at 2^26, build
+    and query of all-identical and Zipf(1.1) keys stay within 4x / 16x of the
+    uniform workload's device time, and the answers are right."""
+    n = 1 << 26
+    uk, uq = _device_keys("uniform", n, 0), _device_keys("uniform", n, 0x51)
+    bu, ut = _device_ms(lambda: hg.build(uk, 1.0))
+    qu, _ = _device_ms(lambda: hg.intersect(ut, uq))
+    sk, sq = _device_keys(kind, n, 1), _device_keys(kind, n, 2)
+    bs, st = _device_ms(lambda: hg.build(sk, 1.0))
+    qs, res = _device_ms(lambda: hg.intersect(st, sq))
+    assert bs <= 4 * bu, (bs, bu)
+    assert qs <= 16 * qu, (qs, qu)
+    if kind == "identical":
+        assert res.matched_positions == n and res.total_matches == n * n
+    else:  # sampled exact check against the oracle's counting rule (tests/oracles.py:25-29)
+        hk, hq = sk.cpu().numpy().view(np.uint32), sq.cpu().numpy().view(np.uint32)
+        pick = np.random.default_rng(3).choice(n, 4096, replace=False)
+        want = O.count_occurrences(hk, hq[pick])
+        assert np.array_equal(res.multiplicities[pick], want)
+
+
+@pytest.mark.parametrize("d", [1024, 1 << 16])
+def test_dense_tables_query_within_bounds(d):
+    """Hash ranges far below the key count (the hash-table path): the query
+    stays within 16x of the uniform one (the reference is O(log d) per query,
+    query.py:102-117)."""
+    n = 1 << 26
+    uk, uq = _device_keys("uniform", n, 0), _device_keys("uniform", n, 0x51)
+    ut = hg.build(uk, 1.0)
+    qu, _ = _device_ms(lambda: hg.intersect(ut, uq))
+    dt = hg.build(uk, 1.0, hash_range=n // d)
+    qd, res = _device_ms(lambda: hg.intersect(dt, uq))
+    assert qd <= 16 * qu, (qd, qu)
+    ref = hg.intersect(ut, uq)  # multiplicities do not depend on the hash range
+    assert np.array_equal(res.multiplicities, ref.multiplicities)
