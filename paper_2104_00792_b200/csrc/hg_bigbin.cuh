@@ -262,7 +262,7 @@ constexpr uint32_t kProbeChunk = 32768;  // queries per shared-memory probe work
 // One thread per fine bin f with queries (tn table keys, qn queries).  A bin
 // whose table slice fits smem (or a medium slice, <= 4 kCap keys: the slice
 // map) is probed by CTA f (its first kProbeChunk queries) plus one extra work
-// item per further chunk (item = f | c << 15); a larger slice goes to the
+// item per further chunk (item = the pair f, c); a larger slice goes to the
 // hash-table path (big_bin list; k_local_probe adds medium slices with too
 // many distinct keys).  List order is free: every consumer works from the
 // lists as written.
@@ -281,7 +281,10 @@ __global__ void k_probe_plan(const uint32_t* __restrict__ t_off, const uint32_t*
   } else if (qn > kProbeChunk) {
     const uint32_t k = (qn + kProbeChunk - 1) / kProbeChunk;
     const uint32_t base = (uint32_t)atomicAdd(plan + kPlanItems, (unsigned long long)(k - 1));
-    for (uint32_t c = 1; c < k; c++) item_x[base + c - 1] = f | (c << 15);
+    for (uint32_t c = 1; c < k; c++) {  // item = (bin, chunk) word pair
+      item_x[2 * (base + c - 1)] = f;
+      item_x[2 * (base + c - 1) + 1] = c;
+    }
   }
 }
 

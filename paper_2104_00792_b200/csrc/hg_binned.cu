@@ -34,10 +34,10 @@ namespace hg {
 
 constexpr int kT = 512;          // threads per CTA; two CTAs per SM
 constexpr int kW = kT / 32;      // warps per CTA
-constexpr int kSub = 128;        // level-2 fan-out (fine bins per level-1 bin)
-constexpr int kSubBits = 7;
+constexpr int kSub = 128;        // level-2 fan-out (fine bins per level-1 bin) up to 32768 fine bins
+constexpr int kSubMax = 256;     // ... and up to 65536 (e.g. 2^30 keys at C = 1 on one GPU): runs half as long
 constexpr int kMaxBins = 256;    // bins one partition tile can split into (8-bit bin ids)
-constexpr uint32_t kMaxFine = kSub * kMaxBins;  // 32768
+constexpr uint32_t kMaxFine = kSubMax * kMaxBins;  // 65536
 
 template <typename K>
 struct TileShape {
@@ -76,10 +76,11 @@ bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLa
   L->s = s;
   L->nfine = (uint32_t)F;
   L->two_level = F > (uint64_t)kSub;
-  L->group = L->two_level ? kSub : 1;
+  L->sub = F > (uint64_t)kSub * kMaxBins ? kSubMax : kSub;
+  L->group = L->two_level ? L->sub : 1;
   L->nb1 = (uint32_t)((F + L->group - 1) / L->group);
   L->bits1 = ceil_log2(L->nb1);
-  L->shift1 = s + (L->two_level ? kSubBits : 0);
+  L->shift1 = s + (L->two_level ? ceil_log2(L->sub) : 0);
   L->tile = key_bits == 32 ? 8192u : 4096u;  // == TileShape<K>::kTile
   L->grid = (uint32_t)num_sms() * 2;
   const uint64_t per = (n + L->grid - 1) / L->grid;
@@ -258,13 +259,28 @@ __device__ __forceinline__ bool load_tile(const K* __restrict__ src, uint32_t m,
 
 // --------------------------------------------------------------------------- pass A
 
-template <typename H>
+template <bool kSplit>
+__device__ __forceinline__ void hist_add_t(uint32_t* s_h, uint32_t f_lo, uint32_t nf, uint32_t f) {
+  if (!kSplit) atomicAdd(s_h + f, 1u);
+  else if (f - f_lo < nf) atomicAdd(s_h + f - f_lo, 1u);
+}
+#define hist_add(...) hist_add_t<kSplit>(__VA_ARGS__)
+
+// kSplit (more than kHistMax fine bins): this launch counts only fine bins
+// [f_lo, f_lo + nf) (one smem counter each); the caller launches once per range.
+constexpr uint32_t kHistMax = 32768;
+
+template <typename H, bool kSplit>
 __global__ void __launch_bounds__(kT)
 k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint32_t nfine, uint32_t group, uint32_t nb1,
-       uint64_t chunk, uint32_t* __restrict__ M, uint32_t* __restrict__ fine_cnt) {
+       uint64_t chunk, uint32_t* __restrict__ M, uint32_t* __restrict__ fine_cnt, uint32_t f_lo, uint32_t nf) {
   using K = typename H::Key;
   extern __shared__ uint32_t s_h[];
-  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) s_h[i] = 0;
+  if (!kSplit) {
+    f_lo = 0;
+    nf = nfine;
+  }
+  for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;
   const uint64_t hi = min(n, lo + chunk);
@@ -280,17 +296,17 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const K* qk = reinterpret_cast<const K*>(&q[u]);
-        atomicAdd(s_h + fine_of<H>(qk[0], hp, s), 1u);
-        atomicAdd(s_h + fine_of<H>(qk[1], hp, s), 1u);
+        hist_add(s_h, f_lo, nf, fine_of<H>(qk[0], hp, s));
+        hist_add(s_h, f_lo, nf, fine_of<H>(qk[1], hp, s));
       }
     }
     for (; i < nv; i += blockDim.x) {
       uint4 q = __ldcs(p + i);
       const K* qk = reinterpret_cast<const K*>(&q);
-      atomicAdd(s_h + fine_of<H>(qk[0], hp, s), 1u);
-      atomicAdd(s_h + fine_of<H>(qk[1], hp, s), 1u);
+      hist_add(s_h, f_lo, nf, fine_of<H>(qk[0], hp, s));
+      hist_add(s_h, f_lo, nf, fine_of<H>(qk[1], hp, s));
     }
-    for (uint64_t j = lo + nv * 2 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
+    for (uint64_t j = lo + nv * 2 + threadIdx.x; j < hi; j += blockDim.x) hist_add(s_h, f_lo, nf, fine_of<H>(keys[j], hp, s));
   } else if (sizeof(K) == 4 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
     const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
     const uint64_t nv = (hi - lo) / 4;
@@ -301,34 +317,36 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
       for (int u = 0; u < 4; u++) q[u] = __ldcs(p + i + u * blockDim.x);
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        atomicAdd(s_h + fine_of<H>((K)q[u].x, hp, s), 1u);
-        atomicAdd(s_h + fine_of<H>((K)q[u].y, hp, s), 1u);
-        atomicAdd(s_h + fine_of<H>((K)q[u].z, hp, s), 1u);
-        atomicAdd(s_h + fine_of<H>((K)q[u].w, hp, s), 1u);
+        hist_add(s_h, f_lo, nf, fine_of<H>((K)q[u].x, hp, s));
+        hist_add(s_h, f_lo, nf, fine_of<H>((K)q[u].y, hp, s));
+        hist_add(s_h, f_lo, nf, fine_of<H>((K)q[u].z, hp, s));
+        hist_add(s_h, f_lo, nf, fine_of<H>((K)q[u].w, hp, s));
       }
     }
     for (; i < nv; i += blockDim.x) {
       uint4 q = __ldcs(p + i);
-      atomicAdd(s_h + fine_of<H>((K)q.x, hp, s), 1u);
-      atomicAdd(s_h + fine_of<H>((K)q.y, hp, s), 1u);
-      atomicAdd(s_h + fine_of<H>((K)q.z, hp, s), 1u);
-      atomicAdd(s_h + fine_of<H>((K)q.w, hp, s), 1u);
+      hist_add(s_h, f_lo, nf, fine_of<H>((K)q.x, hp, s));
+      hist_add(s_h, f_lo, nf, fine_of<H>((K)q.y, hp, s));
+      hist_add(s_h, f_lo, nf, fine_of<H>((K)q.z, hp, s));
+      hist_add(s_h, f_lo, nf, fine_of<H>((K)q.w, hp, s));
     }
-    for (uint64_t j = lo + nv * 4 + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
+    for (uint64_t j = lo + nv * 4 + threadIdx.x; j < hi; j += blockDim.x) hist_add(s_h, f_lo, nf, fine_of<H>(keys[j], hp, s));
   } else {
-    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) atomicAdd(s_h + fine_of<H>(keys[j], hp, s), 1u);
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) hist_add(s_h, f_lo, nf, fine_of<H>(keys[j], hp, s));
   }
   __syncthreads();
   uint32_t* row = M + (uint64_t)blockIdx.x * nb1;
-  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) {
+  for (uint32_t c = f_lo / group + threadIdx.x; c < nb1 && c * group < f_lo + nf; c += blockDim.x) {
     uint32_t sum = 0;
     const uint32_t f1 = min((c + 1) * group, nfine);
-    for (uint32_t f = c * group; f < f1; f++) sum += s_h[f];
+    for (uint32_t f = c * group; f < f1; f++) sum += s_h[f - f_lo];
     row[c] = sum;
   }
-  for (uint32_t f = threadIdx.x; f < nfine; f += blockDim.x)
-    if (s_h[f]) atomicAdd(fine_cnt + f, s_h[f]);
+  for (uint32_t f = threadIdx.x; f < nf; f += blockDim.x)
+    if (s_h[f]) atomicAdd(fine_cnt + f_lo + f, s_h[f]);
 }
+
+#undef hist_add
 
 // One CTA per level-1 bin: exclusive prefix down its column of per-CTA counts
 // (in place).  All G loads are in flight at once; a thread-per-bin serial walk
@@ -352,6 +370,8 @@ __global__ void __launch_bounds__(1024) k_colscan(uint32_t* __restrict__ M, uint
 // plan).
 constexpr uint32_t kHugeBin = 1u << 16;  // oversized bins above this are built by many CTAs in chunks
 
+constexpr uint32_t kStartsChunk = 32768;  // fine bins k_starts scans per smem round
+
 __global__ void __launch_bounds__(1024)
 k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, uint32_t nb1, uint32_t tile,
          uint32_t cap, uint32_t* __restrict__ fine_start, uint32_t* __restrict__ c_start, uint32_t* __restrict__ tp,
@@ -359,37 +379,44 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
          uint32_t big_chunk, uint32_t* __restrict__ big_cp, uint32_t* __restrict__ big_done, uint32_t* __restrict__ zero,
          uint32_t nzero) {
   for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0;
-  extern __shared__ uint32_t s_a[];  // nfine + nb1 + 1
+  extern __shared__ uint32_t s_a[];  // min(nfine, kStartsChunk)
+  __shared__ uint32_t s_t[kMaxBins + 1];
   __shared__ uint32_t s_big, s_huge;
-  uint32_t* s_t = s_a + nfine;
   if (threadIdx.x == 0) s_big = s_huge = 0;
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
-    const uint32_t t = fine_cnt[i];
-    s_a[i] = t;
-    // oversized bins: medium ones from the front of the list, huge ones
-    // (> kHugeBin keys, built in chunks by many CTAs) from the back
-    if (t > kHugeBin && big_cp) big_list[nfine - 1 - atomicAdd(&s_huge, 1u)] = i;
-    else if (t > cap) big_list[atomicAdd(&s_big, 1u)] = i;
+  // fine bins in rounds of kStartsChunk (a level-1 bin never straddles two:
+  // group divides the round); the scan carries across rounds
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nfine; base += kStartsChunk) {
+    const uint32_t len = min(kStartsChunk, nfine - base);
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint32_t t = fine_cnt[base + i];
+      s_a[i] = t;
+      // oversized bins: medium ones from the front of the list, huge ones
+      // (> kHugeBin keys, built in chunks by many CTAs) from the back
+      if (t > kHugeBin && big_cp) big_list[nfine - 1 - atomicAdd(&s_huge, 1u)] = base + i;
+      else if (t > cap) big_list[atomicAdd(&s_big, 1u)] = base + i;
+    }
+    __syncthreads();
+    const uint32_t tot = block_exscan_rows(s_a, len, carry);  // warp-row layout: no bank conflicts
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      fine_start[base + i] = s_a[i];
+      fine_cursor[base + i] = s_a[i];
+    }
+    for (uint32_t c = base / group + threadIdx.x; c < nb1 && c * group < base + len; c += blockDim.x)
+      c_start[c] = s_a[c * group - base];
+    carry += tot;
+    __syncthreads();
   }
-  __syncthreads();
-  const uint32_t total = block_exscan_rows(s_a, nfine, 0);  // warp-row layout: no bank conflicts
-  for (uint32_t i = threadIdx.x; i < nfine; i += blockDim.x) {
-    fine_start[i] = s_a[i];
-    fine_cursor[i] = s_a[i];
-  }
+  const uint32_t total = carry;
   if (threadIdx.x == 0) {
     fine_start[nfine] = total;
+    c_start[nb1] = total;
     big_count[0] = s_big;
     big_count[1] = s_huge;
   }
-  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) {
-    const uint32_t a = s_a[c * group];
-    const uint32_t b = (c + 1) * group < nfine ? s_a[(c + 1) * group] : total;
-    c_start[c] = a;
-    s_t[c] = (b - a + tile - 1) / tile;
-  }
-  if (threadIdx.x == 0) c_start[nb1] = total;
+  __syncthreads();  // c_start (global, this CTA's writes) complete
+  for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) s_t[c] = (c_start[c + 1] - c_start[c] + tile - 1) / tile;
   __syncthreads();
   const uint32_t ntiles = block_exscan(s_t, nb1);
   for (uint32_t c = threadIdx.x; c < nb1; c += blockDim.x) tp[c] = s_t[c];
@@ -397,21 +424,20 @@ k_starts(const uint32_t* __restrict__ fine_cnt, uint32_t nfine, uint32_t group, 
   // oversized bins (hg_bigbin.cuh): chunk prefix, completion counters
   const uint32_t nbig = s_huge;
   if (big_cp == nullptr || nbig == 0) return;
-  uint32_t carry = 0;
+  uint32_t ccarry = 0;
   for (uint32_t base = 0; base < nbig; base += blockDim.x) {
     const uint32_t j = base + threadIdx.x;
     uint32_t c = 0;
     if (j < nbig) {
       const uint32_t f = big_list[nfine - 1 - j];
-      const uint32_t hi = f + 1 < nfine ? s_a[f + 1] : total;
-      c = (hi - s_a[f] + big_chunk - 1) / big_chunk;
+      c = (fine_start[f + 1] - fine_start[f] + big_chunk - 1) / big_chunk;
     }
     uint32_t tot;
     const uint32_t e = block_scan_excl<uint32_t>(c, tot);
-    if (j < nbig) big_cp[j] = carry + e;
-    carry += tot;
+    if (j < nbig) big_cp[j] = ccarry + e;
+    ccarry += tot;
   }
-  if (threadIdx.x == 0) big_cp[nbig] = carry;
+  if (threadIdx.x == 0) big_cp[nbig] = ccarry;
   for (uint32_t j = threadIdx.x; j < nbig; j += blockDim.x) {
     big_done[j] = 0;              // k_big_count
     big_done[nfine + 1 + j] = 0;  // k_big_place
@@ -656,7 +682,7 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
 // tile (the input buffer carries 16 bytes of tail padding).
 template <typename H, bool kQuery>
 __global__ void __launch_bounds__(kT, 2)
-k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
+k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t sub, uint32_t nb1, const uint32_t* __restrict__ c_start,
         const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, KeyOf<H>* __restrict__ out,
         uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
   using K = typename H::Key;
@@ -715,24 +741,24 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     uint32_t bp[KPT / 4];
 #pragma unroll
     for (int k = 0; k < KPT; k++) {
-      const uint32_t b = (uint32_t)(H::bucket(kv[k], hp) >> s_log) & (kSub - 1);
+      const uint32_t b = (uint32_t)(H::bucket(kv[k], hp) >> s_log) & (sub - 1);
       if ((k & 3) == 0) bp[k >> 2] = 0;
       bp[k >> 2] |= b << ((k & 3) * 8);
     }
-    if (threadIdx.x < kSub) tma_store_wait_read();
+    if (threadIdx.x < sub) tma_store_wait_read();
     fence_proxy_async();
     __syncthreads();  // raw and s_loc consumed by every thread
     if (threadIdx.x == 0 && t + gridDim.x < ntiles) locate_issue(t + gridDim.x);
     uint32_t rk[KPT / 2];
-    rank_tile<K, KPT, false>(s, bp, rk, kQuery ? m : s_cur[2], kSub, fine_cursor + (kQuery ? c : s_cur[0]) * kSub);
+    rank_tile<K, KPT, false>(s, bp, rk, kQuery ? m : s_cur[2], sub, fine_cursor + (kQuery ? c : s_cur[0]) * sub);
     if (kQuery) {
-      if (threadIdx.x < kSub) meta[(uint64_t)t * (2 * kSub + 1) + threadIdx.x] = s.dst[threadIdx.x];
-      for (uint32_t i = threadIdx.x; i <= kSub; i += blockDim.x) meta[(uint64_t)t * (2 * kSub + 1) + kSub + i] = s.toff[i];
+      if (threadIdx.x < sub) meta[(uint64_t)t * (2 * sub + 1) + threadIdx.x] = s.dst[threadIdx.x];
+      for (uint32_t i = threadIdx.x; i <= sub; i += blockDim.x) meta[(uint64_t)t * (2 * sub + 1) + sub + i] = s.toff[i];
     }
     place_tile<K, KPT, false>(s, kv, bp, rk, kQuery ? m : s_cur[2], kQuery ? pmap + t0 : nullptr);
-    store_runs<K>(s, kSub, out);
+    store_runs<K>(s, sub, out);
   }
-  if (threadIdx.x < kSub) tma_store_wait_all();
+  if (threadIdx.x < sub) tma_store_wait_all();
 }
 
 // Reverse of a partition level for per-query uint32 values.  Level 2: tiles
@@ -746,7 +772,7 @@ constexpr uint32_t kUnpStaged = 8192 + kPadTotal;
 template <int kLevel>
 __global__ void __launch_bounds__(kT, 2)
 k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
-         const uint32_t* __restrict__ meta, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
+         const uint32_t* __restrict__ meta, uint32_t sub, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
          const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
   constexpr int VPT = 8192 / kT;  // gathered values per thread (tile <= 8192)
   constexpr uint32_t TO = kMaxBins + 1;
@@ -756,7 +782,7 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
   uint32_t* toff = staged + 2 * kUnpStaged;                           // 2 x (kMaxBins + 1)
   uint32_t* base = toff + 2 * TO;                                     // 2 x kMaxBins
   uint32_t* tps = base + 2 * kMaxBins;                                // kMaxBins + 1
-  const uint32_t nbb = kLevel == 1 ? nb : kSub;
+  const uint32_t nbb = kLevel == 1 ? nb : sub;
   uint64_t lo = 0, hi = 0;
   uint32_t ntiles = 0;
   if (threadIdx.x == 0) {
@@ -804,8 +830,8 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
     if (kLevel == 1) {
       if (x <= nb) r0 = meta[tix * (nb + 1) + x];
     } else {
-      if (x < kSub) r1 = meta[tix * (2 * kSub + 1) + x];
-      if (x <= kSub) r0 = meta[tix * (2 * kSub + 1) + kSub + x];
+      if (x < sub) r1 = meta[tix * (2 * sub + 1) + x];
+      if (x <= sub) r0 = meta[tix * (2 * sub + 1) + sub + x];
     }
   };
   // registers -> buffer bf; level-1 bases chain from the previous tile (bf ^ 1)
@@ -819,8 +845,8 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
                                          : base[(bf ^ 1) * kMaxBins + x] + toff[pb + x + 1] - toff[pb + x];
       }
     } else {
-      if (x < kSub) base[bf * kMaxBins + x] = r1;
-      if (x <= kSub) toff[bf * TO + x] = r0;
+      if (x < sub) base[bf * kMaxBins + x] = r1;
+      if (x <= sub) toff[bf * TO + x] = r0;
     }
   };
   // one thread per bin: the run's 16-byte-aligned superset in one bulk copy
@@ -1515,9 +1541,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   if (f >= nfine) {                // further chunks of hot bins
     const uint32_t x = f - nfine;
     if (x >= plan[kPlanItems]) return;
-    const uint32_t it = item_x[x];
-    f = it & 0x7FFFu;
-    c = it >> 15;
+    f = item_x[2 * x];
+    c = item_x[2 * x + 1];
   }
   const uint32_t qlo = q_start[f] + c * kProbeChunk;
   uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
@@ -1697,9 +1722,9 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query,
     b += align_up(n * kb, 256);                          // level-2 output
     b += 2 * align_up(n * 2, 256);                       // pmap1, pmap2
     b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
-    b += align_up(L.max_tiles2 * (2 * kSub + 1) * 4, 256);  // meta2
+    b += align_up(L.max_tiles2 * (2 * L.sub + 1) * 4, 256);  // meta2
     b += align_up(n * 4 + 16, 256);                      // bin-ordered multiplicities (+ tail padding)
-    b += align_up((n / kProbeChunk + 1) * 4, 256);     // extra probe items
+    b += align_up((n / kProbeChunk + 1) * 8, 256);     // extra probe items
     b += 3 * align_up(((size_t)L.nfine + 1) * 4, 256);   // hash-table bins, their table / query prefixes
     b += align_up(kPlanWords * 8, 256);                  // plan
     const uint64_t hs = ht_slots(n_table, key_bits);
@@ -1756,19 +1781,27 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
     po->pmap1 = ws.take<uint16_t>(n);
     po->pmap2 = L.two_level ? ws.take<uint16_t>(n) : nullptr;
     po->meta1 = ws.take<uint32_t>(L.ntiles1 * (L.nb1 + 1));
-    po->meta2 = L.two_level ? ws.take<uint32_t>(L.max_tiles2 * (2 * kSub + 1)) : nullptr;
+    po->meta2 = L.two_level ? ws.take<uint32_t>(L.max_tiles2 * (2 * L.sub + 1)) : nullptr;
   } else {
     out2 = final_out;
   }
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small (%zu < %zu)", ws.cap, ws.used);
   HG_CHECK_CUDA(cudaMemsetAsync(fine_cnt, 0, 4 * (size_t)L.nfine, st));
-  const size_t smA = (size_t)L.nfine * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
-  HG_LAUNCH("hg_hist", k_hist<H>, L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk, po->M,
-            fine_cnt);
+  if (L.nfine <= kHistMax) {
+    const size_t smA = (size_t)L.nfine * 4;
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+    HG_LAUNCH("hg_hist", (k_hist<H, false>), L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk,
+              po->M, fine_cnt, 0u, L.nfine);
+  } else {  // more fine bins than one smem histogram holds: one pass per range
+    const size_t smA = (size_t)kHistMax * 4;
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+    for (uint32_t f_lo = 0; f_lo < L.nfine; f_lo += kHistMax)
+      HG_LAUNCH("hg_hist", (k_hist<H, true>), L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk,
+                po->M, fine_cnt, f_lo, std::min<uint32_t>(kHistMax, L.nfine - f_lo));
+  }
   HG_LAUNCH("hg_colscan", k_colscan, L.nb1, (L.grid + 31) / 32 * 32 > 1024 ? 1024 : (L.grid + 31) / 32 * 32,
             (size_t)L.grid * 4, st, po->M, L.grid, L.nb1);
-  const size_t smS = ((size_t)L.nfine + L.nb1 + 1) * 4;
+  const size_t smS = (size_t)std::min<uint32_t>(L.nfine, kStartsChunk) * 4;
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smS));
   HG_LAUNCH("hg_starts", k_starts, 1, 1024, smS, st, fine_cnt, L.nfine, L.group, L.nb1, L.tile, cap, po->fine_start,
             po->c_start, po->tp, fine_cursor, po->big_list, po->big_count, (uint32_t)BigShape<K>::kChunk, po->big_cp,
@@ -1786,11 +1819,11 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   if (L.two_level) {
     if (query) {
       HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2_q", (k_part2<H, true>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+      HG_LAUNCH("hg_part2_q", (k_part2<H, true>), L.grid, kT, smP, st, out1, hp, L.s, L.sub, L.nb1, po->c_start, po->tp,
                 fine_cursor, out2, po->pmap2, po->meta2);
     } else {
       HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2", (k_part2<H, false>), L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp,
+      HG_LAUNCH("hg_part2", (k_part2<H, false>), L.grid, kT, smP, st, out1, hp, L.s, L.sub, L.nb1, po->c_start, po->tp,
                 fine_cursor, out2, nullptr, nullptr);
     }
     po->grouped = out2;
@@ -1839,7 +1872,7 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   if (split) HG_CHECK_CUDA(cudaEventRecord(split, st));  // query-side grouping done (intersect_timed's split)
   uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
   const uint32_t max_extra = (uint32_t)(q / kProbeChunk + 1);
-  uint32_t* item_x = ws.take<uint32_t>(max_extra);
+  uint32_t* item_x = ws.take<uint32_t>(2 * (size_t)max_extra);
   uint32_t* big_bin = ws.take<uint32_t>(L.nfine + 1);
   uint32_t* big_t = ws.take<uint32_t>(L.nfine + 1);
   uint32_t* big_q = ws.take<uint32_t>(L.nfine + 1);
@@ -1866,13 +1899,13 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
   if (L.two_level) {
     HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
-    HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, mult_bo, level1_vals, po.pmap2, po.meta2, L.nb1, L.tile,
+    HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, mult_bo, level1_vals, po.pmap2, po.meta2, L.sub, L.nb1, L.tile,
               q, L.chunk, po.M, po.c_start, po.tp);
   } else {
     level1_vals = mult_bo;
   }
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
-  HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.nb1, L.tile, q,
+  HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.sub, L.nb1, L.tile, q,
             L.chunk, po.M, po.c_start, po.tp);
   return HG_OK;
 }

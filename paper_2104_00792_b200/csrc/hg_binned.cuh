@@ -11,7 +11,8 @@ struct BinLayout {
   uint32_t nb1;        // level-1 bins (F when one level)
   int bits1;           // ballot bits for level 1
   int shift1;          // level-1 bin = bucket >> shift1
-  uint32_t group;      // fine bins per level-1 bin (1 or 128)
+  uint32_t group;      // fine bins per level-1 bin (1 or sub)
+  uint32_t sub;        // level-2 fan-out: 128, or 256 above 32768 fine bins
   uint32_t grid;       // CTAs of A / P1 / R1 (one chunk each)
   uint64_t chunk;      // keys per chunk (multiple of the tile)
   uint32_t tile;
