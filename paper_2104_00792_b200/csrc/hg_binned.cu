@@ -680,9 +680,9 @@ k_part1(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int shift1
 // level-1 order) and meta = [128 claims | 129 tile offsets] per tile.  Tiles
 // start anywhere, so the TMA copy starts at the 16-byte boundary below the
 // tile (the input buffer carries 16 bytes of tail padding).
-template <typename H, bool kQuery>
+template <typename H, bool kQuery, uint32_t sub>  // sub = level-2 fan-out (128 or 256), compile-time
 __global__ void __launch_bounds__(kT, 2)
-k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t sub, uint32_t nb1, const uint32_t* __restrict__ c_start,
+k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
         const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, KeyOf<H>* __restrict__ out,
         uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
   using K = typename H::Key;
@@ -1817,15 +1817,19 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
               po->M, po->c_start, out1, nullptr, nullptr);
   }
   if (L.two_level) {
-    if (query) {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2_q", (k_part2<H, true>), L.grid, kT, smP, st, out1, hp, L.s, L.sub, L.nb1, po->c_start, po->tp,
-                fine_cursor, out2, po->pmap2, po->meta2);
-    } else {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_part2<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
-      HG_LAUNCH("hg_part2", (k_part2<H, false>), L.grid, kT, smP, st, out1, hp, L.s, L.sub, L.nb1, po->c_start, po->tp,
-                fine_cursor, out2, nullptr, nullptr);
-    }
+    auto part2 = [&](auto kern, const char* name, uint16_t* pm, uint32_t* mt) -> int {
+      HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_LAUNCH(name, kern, L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp, fine_cursor, out2, pm, mt);
+      return HG_OK;
+    };
+    int rc2;
+    if (query)
+      rc2 = L.sub == kSub ? part2(k_part2<H, true, kSub>, "hg_part2_q", po->pmap2, po->meta2)
+                          : part2(k_part2<H, true, kSubMax>, "hg_part2_q", po->pmap2, po->meta2);
+    else
+      rc2 = L.sub == kSub ? part2(k_part2<H, false, kSub>, "hg_part2", nullptr, nullptr)
+                          : part2(k_part2<H, false, kSubMax>, "hg_part2", nullptr, nullptr);
+    if (rc2) return rc2;
     po->grouped = out2;
   } else {
     po->grouped = out1;
