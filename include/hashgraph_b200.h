@@ -71,6 +71,12 @@ HG_API int hg_hash(const void* keys, uint64_t n, int key_bits, int kind, uint32_
  * unspecified, core.py:12-14); positions (nullable): uint32[n], input index of
  * the key at each edge slot. */
 HG_API size_t hg_build_workspace_size(uint64_t n, uint64_t v, int key_bits);
+/* Workspace for hg_build with positions on the binned path (build_traced):
+ * the workspace then also holds the build's TRACE (position maps of both
+ * partition levels and each grouped key's edge slot), which
+ * hg_intersect_tables reuses to return counts to input order by streaming
+ * instead of scattering.  A smaller workspace runs the direct Alg. 1 kernels. */
+HG_API size_t hg_build_traced_workspace_size(uint64_t n, uint64_t v, int key_bits);
 HG_API int hg_build(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t v,
              uint32_t* offsets, void* edges, uint32_t* positions, void* workspace,
              size_t workspace_bytes, void* stream);
@@ -83,6 +89,21 @@ HG_API int hg_build(const void* keys, uint64_t n, int key_bits, int kind, uint32
 HG_API int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const uint32_t* offsets_b,
                  const void* edges_b, const uint32_t* positions_b, uint64_t n_b, int key_bits,
                  int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* stream);
+
+/* intersect_tables on the binned path (query.py:120-179): the query table's
+ * fine-bin slices are probed against table A (the same depth classes,
+ * sorted-bucket search and hash-table path as hg_query), counts return to
+ * query order through `trace` (the workspace of the hg_build that produced
+ * table B with positions, hg_build_traced_workspace_size bytes; nullable) or,
+ * without a trace, by scattering through positions_b.  n_a = table A's key
+ * count.  Small inputs run hg_intersect's kernels.  agg accumulated (caller
+ * zeroes). */
+HG_API size_t hg_intersect_tables_workspace_size(uint64_t n_b, uint64_t v, uint64_t n_a, int key_bits);
+HG_API int hg_intersect_tables(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a,
+                        const uint32_t* offsets_b, const void* edges_b, const uint32_t* positions_b,
+                        uint64_t n_b, int key_bits, int kind, uint32_t seed, uint64_t v, void* trace,
+                        size_t trace_bytes, uint32_t* mult, uint64_t* agg, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* Whole query against a built table -- replaces query.intersect /
  * intersect_timed (query.py:182-202): builds the query-side table with the

@@ -33,10 +33,14 @@ SIGNATURES = {
     "hg_timing_collect": (_c_int, [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _c_int]),
     "hg_hash": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_ptr, _c_int, _c_ptr]),
     "hg_build_workspace_size": (_c_size, [_c_u64, _c_u64, _c_int]),
+    "hg_build_traced_workspace_size": (_c_size, [_c_u64, _c_u64, _c_int]),
     "hg_build": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
                           _c_size, _c_ptr]),
     "hg_intersect": (_c_int, [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64,
                               _c_ptr, _c_ptr, _c_ptr]),
+    "hg_intersect_tables_workspace_size": (_c_size, [_c_u64, _c_u64, _c_u64, _c_int]),
+    "hg_intersect_tables": (_c_int, [_c_ptr, _c_ptr, _c_u64, _c_ptr, _c_ptr, _c_ptr, _c_u64, _c_int, _c_int, _c_u32,
+                                     _c_u64, _c_ptr, _c_size, _c_ptr, _c_ptr, _c_ptr, _c_size, _c_ptr]),
     "hg_query_workspace_size": (_c_size, [_c_u64, _c_u64, _c_u64, _c_int]),
     "hg_query": (_c_int, [_c_ptr, _c_ptr, _c_u64, _c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_ptr, _c_ptr,
                           _c_ptr, _c_size, _c_ptr]),

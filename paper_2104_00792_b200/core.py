@@ -49,7 +49,7 @@ class HashGraph:
     """The CSR pair plus the parameters that produced it; immutable (core.py:58-81)."""
 
     __slots__ = ("offset_device", "keys_device", "hash_range", "family", "load_factor", "key_bits",
-                 "_num_keys", "_offset", "_keys", "_frozen")
+                 "_num_keys", "_offset", "_keys", "_frozen", "_trace")
 
     def __init__(self, offset_device, keys_device, hash_range: int, family, load_factor: float,
                  key_bits: int = 32, num_keys: int | None = None):
@@ -62,6 +62,7 @@ class HashGraph:
         object.__setattr__(self, "_num_keys", int(keys_device.numel() if num_keys is None else num_keys))
         object.__setattr__(self, "_offset", None)
         object.__setattr__(self, "_keys", None)
+        object.__setattr__(self, "_trace", None)  # QueryTableTrace of a build_query_table table
         object.__setattr__(self, "_frozen", True)
 
     def __setattr__(self, name, value):
@@ -127,10 +128,12 @@ def _resolve_range(n: int, load_factor: float, hash_range) -> int:
     return int(hash_range)
 
 
-def build_device(keys_dev, v: int, family, key_bits: int = 32, want_positions: bool = False):
+def build_device(keys_dev, v: int, family, key_bits: int = 32, want_positions: bool = False, keep_trace: bool = False):
     """Launch the GPU build over device keys: (offset u32[v+1], edges, positions u32 | None).
 
-    Enqueue-only on the current stream."""
+    Enqueue-only on the current stream.  With positions the binned path runs
+    traced (hg_build_traced_workspace_size); keep_trace also returns the
+    workspace, which then holds the trace hg_intersect_tables reuses."""
     t = D.torch()
     n = keys_dev.numel()
     kind, seed = family_code(family)
@@ -138,9 +141,13 @@ def build_device(keys_dev, v: int, family, key_bits: int = 32, want_positions: b
         offsets = t.empty(v + 1, dtype=t.int32, device=keys_dev.device)
         edges = t.empty(n, dtype=keys_dev.dtype, device=keys_dev.device)
         positions = t.empty(n, dtype=t.int32, device=keys_dev.device) if want_positions else None
-        ws = D.workspace(_lib.load().hg_build_workspace_size(n, v, key_bits))
+        size = (_lib.load().hg_build_traced_workspace_size if want_positions else
+                _lib.load().hg_build_workspace_size)(n, v, key_bits)
+        ws = D.workspace(size)
         _lib.call("hg_build", D.ptr(keys_dev), n, key_bits, kind, seed, v, D.ptr(offsets), D.ptr(edges),
                   D.ptr(positions), D.ptr(ws), ws.numel(), D.stream_ptr())
+    if keep_trace:
+        return offsets, edges, positions, ws
     return offsets, edges, positions
 
 
@@ -166,7 +173,7 @@ def build_traced(keys, load_factor: float = 1.0, family: HashFamily = HashFamily
     return table, counters, positions
 
 
-def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_positions):
+def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_positions, keep_trace=False):
     if key_bits not in (32, 64):
         raise ConfigError(f"key_bits must be 32 or 64, got {key_bits}")
     if not D.is_tensor(keys):
@@ -176,9 +183,16 @@ def _build(keys, load_factor, family, worker_count, hash_range, key_bits, want_p
     n = D.key_count(keys)
     v = _resolve_range(n, load_factor, hash_range)
     dk = D.to_device_keys(keys, key_bits)
-    offsets, edges, positions = build_device(dk, v, family, key_bits, want_positions)
+    if keep_trace:
+        offsets, edges, positions, trace = build_device(dk, v, family, key_bits, want_positions, True)
+    else:
+        offsets, edges, positions = build_device(dk, v, family, key_bits, want_positions)
+        trace = None
     table = HashGraph(offsets, edges, v, family, float(load_factor), key_bits, n)
-    return table, BuildCounters(hashed=n, counted=n, placed=n), positions
+    counters = BuildCounters(hashed=n, counted=n, placed=n)
+    if keep_trace:
+        return table, counters, positions, trace
+    return table, counters, positions
 
 
 # ---------------------------------------------------------------- snapshots (core.py:27-28, 212-255)

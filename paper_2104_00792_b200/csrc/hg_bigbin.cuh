@@ -86,7 +86,8 @@ template <typename H>
 __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, KeyOf<H>* __restrict__ dst, int copy,
                                            uint32_t lo, uint32_t hi, uint64_t first, const HashParams& hp, int s,
                                            uint64_t v, uint32_t* cnt, uint32_t* __restrict__ offsets,
-                                           KeyOf<H>* __restrict__ edges) {
+                                           KeyOf<H>* __restrict__ edges, const uint32_t* __restrict__ a2,
+                                           uint32_t* __restrict__ positions, uint32_t* __restrict__ lmap) {
   using K = KeyOf<H>;
   const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
   const uint32_t lt = lanemask_lt();
@@ -131,7 +132,15 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
       uint32_t b0 = 0;
       if (ok && (peers & lt) == 0) b0 = atomicAdd(cnt + l, (uint32_t)__popc(peers));
       b0 = __shfl_sync(0xffffffffu, b0, __ffs(peers) - 1);
-      if (ok) edges[b0 + __popc(peers & lt)] = kv[u];
+      if (ok) {
+        const uint32_t slot = b0 + __popc(peers & lt);
+        edges[slot] = kv[u];
+        if (a2) {  // traced build
+          const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+          positions[slot] = a2[e];
+          lmap[e] = slot;
+        }
+      }
     }
   }
   __syncthreads();
@@ -143,7 +152,9 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
                                                     const uint32_t* __restrict__ huge_list,
                                                     const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_cp,
                                                     uint32_t* __restrict__ done, HashParams hp, int s, uint64_t v,
-                                                    uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges) {
+                                                    uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges,
+                                                    const uint32_t* __restrict__ a2, uint32_t* __restrict__ positions,
+                                                    uint32_t* __restrict__ lmap) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
@@ -153,7 +164,8 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
   const uint32_t lt = lanemask_lt();
   for (uint32_t k = blockIdx.x; k < nmed; k += gridDim.x) {
     const uint32_t f = big_list[k];
-    big_medium<H>(src, dst, copy, fine_start[f], fine_start[f + 1], (uint64_t)f << s, hp, s, v, cnt, offsets, edges);
+    big_medium<H>(src, dst, copy, fine_start[f], fine_start[f + 1], (uint64_t)f << s, hp, s, v, cnt, offsets, edges, a2,
+                  positions, lmap);
   }
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
     big_chunk(k, nbig, BS::kChunk, big_cp, huge_list, fine_start, s_loc);
@@ -200,7 +212,8 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
                                                     const uint32_t* __restrict__ huge_list, const uint32_t* __restrict__ big_count,
                                                     const uint32_t* __restrict__ big_cp, uint32_t* __restrict__ done,
                                                     HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets,
-                                                    KeyOf<H>* __restrict__ edges) {
+                                                    KeyOf<H>* __restrict__ edges, const uint32_t* __restrict__ a2,
+                                                    uint32_t* __restrict__ positions, uint32_t* __restrict__ lmap) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
@@ -242,7 +255,15 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++)
-      if (lr[u] != 0xFFFFFFFFu) edges[cnt[lr[u] >> 15] + (lr[u] & 0x7FFFu)] = kv[u];
+      if (lr[u] != 0xFFFFFFFFu) {
+        const uint32_t slot = cnt[lr[u] >> 15] + (lr[u] & 0x7FFFu);
+        edges[slot] = kv[u];
+        if (a2) {  // traced build
+          const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+          positions[slot] = a2[e];
+          lmap[e] = slot;
+        }
+      }
     if (last_chunk(done, j, nck)) {
       for (uint32_t l = threadIdx.x; l < nb; l += blockDim.x) cnt[l] = __ldcg(offsets + first + l);
       __syncthreads();

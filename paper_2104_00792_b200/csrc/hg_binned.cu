@@ -937,6 +937,76 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
   }
 }
 
+// Forward of a partition level for per-key uint32 values (the inverse of
+// k_unpart): each tile's values (input order; level 1 with vals == nullptr:
+// the input index itself) go to their staged slots through the recorded u16
+// position map, then every run leaves for its recorded destination -- the
+// same permutation k_part1 / k_part2 applied to the keys, with no hashing or
+// ranking.  build_traced uses it to carry input indices to the grouped order.
+template <int kLevel>
+__global__ void __launch_bounds__(kT, 2)
+k_repart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
+         const uint32_t* __restrict__ meta, uint32_t sub, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
+         const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw);  // kUnpStaged
+  __shared__ uint32_t toff[kMaxBins + 1], base[kMaxBins], tps[kMaxBins + 1];
+  const uint32_t nbb = kLevel == 1 ? nb : sub;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t lo = 0, hi = 0;
+  uint32_t ntiles;
+  if (kLevel == 1) {
+    lo = (uint64_t)blockIdx.x * chunk;
+    hi = min(n, lo + chunk);
+    ntiles = hi > lo ? (uint32_t)((hi - lo + tile - 1) / tile) : 0u;
+    for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) base[x] = c_start[x] + M[(uint64_t)blockIdx.x * nb + x];
+  } else {
+    for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) tps[i] = tp_g[i];
+    __syncthreads();
+    const uint32_t tot = tps[nb];
+    ntiles = tot > blockIdx.x ? (tot - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+  }
+  for (uint32_t it = 0; it < ntiles; it++) {
+    uint64_t t0, tix;
+    uint32_t m;
+    if (kLevel == 1) {
+      t0 = lo + (uint64_t)it * tile;
+      m = (uint32_t)min((uint64_t)tile, hi - t0);
+      tix = t0 / tile;
+    } else {
+      const uint32_t t = blockIdx.x + it * gridDim.x;
+      uint32_t a = 0, z = nb;
+      while (z - a > 1) {
+        const uint32_t mid = (a + z) >> 1;
+        if (tps[mid] <= t) a = mid; else z = mid;
+      }
+      t0 = c_start[a] + (t - tps[a]) * tile;
+      m = min(tile, c_start[a + 1] - (uint32_t)t0);
+      tix = t;
+    }
+    for (uint32_t x = threadIdx.x; x <= nbb; x += blockDim.x) {
+      if (kLevel == 1) {
+        toff[x] = meta[tix * (nb + 1) + x];
+      } else {
+        toff[x] = meta[tix * (2 * sub + 1) + sub + x];
+        if (x < sub) base[x] = meta[tix * (2 * sub + 1) + x];
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+      staged[pmap[t0 + i]] = vals ? vals[t0 + i] : (uint32_t)(t0 + i);
+    __syncthreads();
+    for (uint32_t b = warp; b < nbb; b += kT / 32) {  // one warp per run: coalesced stores
+      const uint32_t c0 = toff[b], cnt = toff[b + 1] - c0, d = base[b];
+      const uint32_t p = pad_start(c0, b, d);
+      for (uint32_t k = lane; k < cnt; k += 32) out[d + k] = staged[p + k];
+    }
+    __syncthreads();
+    if (kLevel == 1)
+      for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) base[x] += toff[x + 1] - toff[x];
+    __syncthreads();
+  }
+}
+
 // --------------------------------------------------------------------------- C: local build
 
 // Exclusive scan of the nb packed-u16 bucket counters of a 1024-thread CTA
@@ -1021,10 +1091,14 @@ struct LocalPShape {
   static size_t smem(int s) { return c16_bytes(s) + 2 * (size_t)kChunks * 16; }
 };
 
-template <typename H>
+// kTrace (build_traced / build_query_table): also positions[p] = a2[g] (the
+// input index of grouped key g, from k_repart) and lmap[g] = p for the slot p
+// each grouped key lands in.
+template <typename H, bool kTrace = false>
 __global__ void __launch_bounds__(1024, 1)
 k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
-                uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges) {
+                uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges, const uint32_t* __restrict__ a2 = nullptr,
+                uint32_t* __restrict__ positions = nullptr, uint32_t* __restrict__ lmap = nullptr) {
   using K = typename H::Key;
   using PS = LocalPShape<K>;
   constexpr int NT = PS::kThreads;
@@ -1146,12 +1220,18 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
     __syncthreads();
     K* stg = staged + sh;
-    auto place_key = [&](K key, int k) {
+    auto place_key = [&](K key, int k, uint32_t g) {
+      uint32_t rel;
       if (kRehash) {
         const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
-        stg[get16(c16, l) + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu)] = key;
+        rel = get16(c16, l) + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
       } else {
-        stg[get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu)] = key;
+        rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
+      }
+      stg[rel] = key;
+      if (kTrace) {
+        positions[lo + rel] = a2[g];
+        lmap[g] = lo + rel;
       }
     };
 #pragma unroll
@@ -1161,11 +1241,11 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       if (c < nch) {
         if (e0 >= sh && e0 + VPL <= sh + cnt) {
 #pragma unroll
-          for (int j = 0; j < (int)VPL; j++) place_key(kv[i * VPL + j], i * VPL + j);
+          for (int j = 0; j < (int)VPL; j++) place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
         } else {
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
-            if (e0 + j - sh < cnt) place_key(kv[i * VPL + j], i * VPL + j);
+            if (e0 + j - sh < cnt) place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
         }
       }
     }
@@ -1711,31 +1791,6 @@ static uint64_t ht_slots(uint64_t n_table, int key_bits) {
   return c;
 }
 
-size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query, uint64_t n_table) {
-  const size_t kb = key_bits / 8;
-  size_t b = 0;
-  b += align_up((size_t)L.grid * L.nb1 * 4, 256);        // M
-  b += 4 * align_up(((size_t)L.nfine + 1) * 4, 256);     // fine cnt / start / cursor / big list
-  b += 2 * align_up(((size_t)L.nb1 + 1) * 4, 256) + 256; // c_start, tp, big count
-  b += align_up(n * kb, 256);                            // level-1 output
-  if (query) {
-    b += align_up(n * kb, 256);                          // level-2 output
-    b += 2 * align_up(n * 2, 256);                       // pmap1, pmap2
-    b += align_up(L.ntiles1 * (L.nb1 + 1) * 4, 256);     // meta1
-    b += align_up(L.max_tiles2 * (2 * L.sub + 1) * 4, 256);  // meta2
-    b += align_up(n * 4 + 16, 256);                      // bin-ordered multiplicities (+ tail padding)
-    b += align_up((n / kProbeChunk + 1) * 8, 256);     // extra probe items
-    b += 3 * align_up(((size_t)L.nfine + 1) * 4, 256);   // hash-table bins, their table / query prefixes
-    b += align_up(kPlanWords * 8, 256);                  // plan
-    const uint64_t hs = ht_slots(n_table, key_bits);
-    b += align_up(hs * kb, 256) + align_up(hs * 4, 256);  // hash table keys + counts
-  } else {
-    b += align_up(((size_t)L.nfine + 1) * 4, 256);       // oversized-bin chunk prefix
-    b += align_up(((size_t)L.nfine + 1) * 8, 256);       // their chunk-completion counters
-  }
-  return b + 4096;
-}
-
 struct PartOut {
   const void* grouped;  // keys grouped by fine bin at fine_start positions
   void* out1;           // level-1 buffer (n keys of workspace)
@@ -1754,37 +1809,108 @@ struct PartOut {
   uint32_t* meta2;
 };
 
-// Passes A + P1 (+ P2).  Build mode with two levels writes the fine-grouped
-// keys into `final_out`; otherwise they stay in workspace buffers.
-template <typename H>
-static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap, bool query,
-                         KeyOf<H>* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
-  using K = KeyOf<H>;
-  uint32_t* fine_cnt = ws.take<uint32_t>(L.nfine + 1);
+// Partition modes: kPartBuild (keys grouped straight into the table's edges,
+// oversized-bin lists), kPartQuery (position maps + run metadata for the way
+// back, the probe plan), kPartTraced (build_traced: both maps and lists; the
+// grouped keys stay in workspace and the maps outlive the call as the trace).
+enum PartMode { kPartBuild, kPartQuery, kPartTraced };
+
+// Carve the partition's buffers out of the workspace (also used to re-derive
+// a trace's pointers from its workspace: same order, same sizes).
+template <typename K>
+static void part_alloc(uint64_t n, const BinLayout& L, PartMode mode, K* final_out, Workspace& ws, PartOut* po,
+                       uint32_t** fine_cnt, uint32_t** fine_cursor, K** out2) {
+  const bool maps = mode != kPartBuild, lists = mode != kPartQuery;
+  *fine_cnt = ws.take<uint32_t>(L.nfine + 1);
   po->fine_start = ws.take<uint32_t>(L.nfine + 1);
-  uint32_t* fine_cursor = ws.take<uint32_t>(L.nfine + 1);
+  *fine_cursor = ws.take<uint32_t>(L.nfine + 1);
   po->big_list = ws.take<uint32_t>(L.nfine + 1);
   po->c_start = ws.take<uint32_t>(L.nb1 + 1);
   po->tp = ws.take<uint32_t>(L.nb1 + 1);
   po->big_count = ws.take<uint32_t>(64);
   po->M = ws.take<uint32_t>((size_t)L.grid * L.nb1);
-  po->big_cp = query ? nullptr : ws.take<uint32_t>(L.nfine + 1);
-  po->big_done = query ? nullptr : ws.take<uint32_t>(2 * (size_t)L.nfine + 2);
-  po->plan32 = query ? ws.take<uint32_t>(2 * kPlanWords) : nullptr;
+  po->big_cp = lists ? ws.take<uint32_t>(L.nfine + 1) : nullptr;
+  po->big_done = lists ? ws.take<uint32_t>(2 * (size_t)L.nfine + 2) : nullptr;
+  po->plan32 = mode == kPartQuery ? ws.take<uint32_t>(2 * kPlanWords) : nullptr;
   K* out1 = ws.take<K>(n + 16 / sizeof(K));  // + tail padding for k_part2's TMA
-  K* out2 = nullptr;
   po->out1 = out1;
   po->pmap1 = po->pmap2 = nullptr;
   po->meta1 = po->meta2 = nullptr;
-  if (query) {
-    out2 = L.two_level ? ws.take<K>(n) : nullptr;
+  if (maps) {
+    *out2 = L.two_level ? ws.take<K>(n) : nullptr;
     po->pmap1 = ws.take<uint16_t>(n);
     po->pmap2 = L.two_level ? ws.take<uint16_t>(n) : nullptr;
     po->meta1 = ws.take<uint32_t>(L.ntiles1 * (L.nb1 + 1));
     po->meta2 = L.two_level ? ws.take<uint32_t>(L.max_tiles2 * (2 * L.sub + 1)) : nullptr;
   } else {
-    out2 = final_out;
+    *out2 = final_out;
   }
+  po->grouped = L.two_level ? (const void*)*out2 : (const void*)out1;
+}
+
+// The probe stage's buffers (queries grouped by fine bin -> counts in the
+// same order), carved after the partition's.
+struct ProbeBufs {
+  uint32_t* mult_bo;   // counts in grouped order (+ tail padding for k_unpart's aligned run copies)
+  uint32_t* item_x;    // extra probe work items (bin, chunk) of hot bins
+  uint32_t* big_bin;   // hash-table bins, their table-key / query prefixes
+  uint32_t* big_t;
+  uint32_t* big_q;
+  void* hk;            // hash table keys / counts (ht_slots(n_table))
+  uint32_t* hc;
+  uint32_t max_extra;
+  uint64_t hs;
+};
+
+template <typename K>
+static void probe_alloc(uint64_t q, const BinLayout& L, uint64_t n_table, Workspace& ws, ProbeBufs* pb) {
+  pb->mult_bo = ws.take<uint32_t>(q + 4);
+  pb->max_extra = (uint32_t)(q / kProbeChunk + 1);
+  pb->item_x = ws.take<uint32_t>(2 * (size_t)pb->max_extra);
+  pb->big_bin = ws.take<uint32_t>(L.nfine + 1);
+  pb->big_t = ws.take<uint32_t>(L.nfine + 1);
+  pb->big_q = ws.take<uint32_t>(L.nfine + 1);
+  pb->hs = ht_slots(n_table, sizeof(K) * 8);
+  pb->hk = ws.take<K>(pb->hs);
+  pb->hc = ws.take<uint32_t>(pb->hs);
+}
+
+// Workspace of a binned pass, by a dry run of the same carve-up the pass
+// performs (mode: kPartBuild / kPartQuery / kPartTraced; the query adds its
+// probe buffers, the traced build the carried input indices and lmap).
+template <typename K>
+static size_t ws_dry_run(uint64_t n, const BinLayout& L, PartMode mode, uint64_t n_table) {
+  Workspace w{nullptr, ~(size_t)0, 0};
+  PartOut po{};
+  uint32_t *fc, *fcur;
+  K* out2;
+  part_alloc<K>(n, L, mode, nullptr, w, &po, &fc, &fcur, &out2);
+  if (mode == kPartQuery) {
+    ProbeBufs pb;
+    probe_alloc<K>(n, L, n_table, w, &pb);
+  } else if (mode == kPartTraced) {
+    w.take<uint32_t>(n + 4);  // carried input indices (a2)
+    w.take<uint32_t>(n + 4);  // lmap
+  }
+  return w.used + 4096;
+}
+
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, int mode, uint64_t n_table) {
+  return key_bits == 32 ? ws_dry_run<uint32_t>(n, L, (PartMode)mode, n_table)
+                        : ws_dry_run<uint64_t>(n, L, (PartMode)mode, n_table);
+}
+
+// Passes A + P1 (+ P2).  Build mode with two levels writes the fine-grouped
+// keys into `final_out`; otherwise they stay in workspace buffers.
+template <typename H>
+static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap,
+                         PartMode mode, KeyOf<H>* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
+  using K = KeyOf<H>;
+  const bool query = mode != kPartBuild;  // position maps + metadata
+  uint32_t *fine_cnt, *fine_cursor;
+  K* out2;
+  part_alloc<K>(n, L, mode, final_out, ws, po, &fine_cnt, &fine_cursor, &out2);
+  K* out1 = (K*)po->out1;
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small (%zu < %zu)", ws.cap, ws.used);
   HG_CHECK_CUDA(cudaMemsetAsync(fine_cnt, 0, 4 * (size_t)L.nfine, st));
   if (L.nfine <= kHistMax) {
@@ -1837,31 +1963,86 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   return HG_OK;
 }
 
+// positions != nullptr: build_traced -- the partition also records its
+// position maps (kPartTraced), k_repart carries every key's input index to
+// the grouped order, and the local build writes positions[p] and lmap[g] = p.
+// The workspace then holds the trace hg_intersect_tables reuses.
 template <typename H>
 static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
-                 KeyOf<H>* edges, Workspace& ws, cudaStream_t st) {
+                      KeyOf<H>* edges, Workspace& ws, cudaStream_t st, uint32_t* positions = nullptr) {
   using K = KeyOf<H>;
+  const bool traced = positions != nullptr;
   PartOut po{};
-  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, false, edges, ws, st, &po);
+  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, traced ? kPartTraced : kPartBuild, edges, ws, st, &po);
   if (rc) return rc;
-  const K* grouped = (const K*)po.grouped;  // == edges (two levels) or the level-1 buffer
+  uint32_t *a2 = nullptr, *lmap = nullptr;
+  if (traced) {
+    a2 = ws.take<uint32_t>(n + 4);
+    lmap = ws.take<uint32_t>(n + 4);
+    if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small for a traced build");
+    const size_t smR = (size_t)kUnpStaged * 4;
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_repart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    uint32_t* a1 = L.two_level ? reinterpret_cast<uint32_t*>(po.out1) : a2;  // level-1 keys are dead after part2
+    HG_LAUNCH("hg_repart1", k_repart<1>, L.grid, kT, smR, st, nullptr, a1, po.pmap1, po.meta1, L.sub, L.nb1, L.tile, n,
+              L.chunk, po.M, po.c_start, po.tp);
+    if (L.two_level) {
+      HG_CHECK_CUDA(cudaFuncSetAttribute(k_repart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+      HG_LAUNCH("hg_repart2", k_repart<2>, L.grid, kT, smR, st, a1, a2, po.pmap2, po.meta2, L.sub, L.nb1, L.tile, n,
+                L.chunk, po.M, po.c_start, po.tp);
+    }
+  }
+  const K* grouped = (const K*)po.grouped;  // build: == edges (two levels) or the level-1 buffer; traced: workspace
   const size_t smC = LocalPShape<K>::smem(L.s);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
-  HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
-            L.nfine, hp, L.s, v, offsets, edges);
+  if (traced) {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+    HG_LAUNCH("hg_local_build_traced", (k_local_build_p<H, true>), num_sms(), LocalPShape<K>::kThreads, smC, st, grouped,
+              po.fine_start, L.nfine, hp, L.s, v, offsets, edges, a2, positions, lmap);
+  } else {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+    HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
+              L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr);
+  }
   // oversized fine bins (hg_bigbin.cuh), in chunks over the whole grid: with
-  // two levels their keys sit in edges (in place), so the count pass copies
-  // them to the free level-1 buffer and placement reads them from there
-  K* src = (K*)po.out1;
-  const int copy = L.two_level ? 1 : 0;
+  // two levels (untraced) their keys sit in edges (in place), so the count
+  // pass copies them to the free level-1 buffer and placement reads them
+  // from there
+  const int copy = (L.two_level && !traced) ? 1 : 0;
+  K* src = copy ? (K*)po.out1 : (K*)grouped;
   const size_t smBig = (size_t)(1u << L.s) * 4;
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_count<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
   const uint32_t* huge_list = po.big_list + L.nfine - 1;  // grows downwards (k_starts)
-  HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, src, copy, po.fine_start, po.big_list,
-            huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges);
+  HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, (K*)po.out1, copy, po.fine_start,
+            po.big_list, huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges, a2, positions, lmap);
   HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
   HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, huge_list,
-            po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges);
+            po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges, a2, positions, lmap);
+  return HG_OK;
+}
+
+// The probe of queries already grouped by fine bin (q_start: F + 1 bin
+// starts): shared-memory probe items, then the hash-table path.  `plan`
+// (kPlanWords) must be zero.  Counts land in pb.mult_bo in grouped order.
+template <typename H>
+static int probe_stage(const uint32_t* t_off, const KeyOf<H>* t_edges, const KeyOf<H>* qpart, const uint32_t* q_start,
+                       uint64_t q, const HashParams& hp, uint64_t v, const BinLayout& L, unsigned long long* plan,
+                       ProbeBufs& pb, uint64_t* agg, cudaStream_t st) {
+  using K = KeyOf<H>;
+  (void)q;
+  HG_LAUNCH("hg_probe_plan", k_probe_plan, (L.nfine + 255) / 256, 256, 0, st, t_off, q_start, L.nfine, L.s, v,
+            LocalShape<K>::kCap, pb.item_x, pb.big_bin, plan);
+  const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
+  HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine + pb.max_extra, kT, smQ, st, t_off, t_edges, qpart, q_start,
+            L.nfine, pb.item_x, plan, pb.big_bin, hp, L.s, v, pb.mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  if (pb.hs) {  // oversized table slices: key -> count hash table over the whole grid
+    K* hk = (K*)pb.hk;
+    HG_LAUNCH("hg_ht_prep", k_ht_prep<K>, num_sms() * 4, 256, 0, st, plan, pb.big_bin, t_off, q_start, L.s, v, pb.big_t,
+              pb.big_q, hk, pb.hc);
+    HG_LAUNCH("hg_ht_insert", k_ht_insert<H>, num_sms() * 2, kHtT, 0, st, t_off, t_edges, L.s, v, pb.big_bin, pb.big_t,
+              plan, hk, pb.hc);
+    HG_LAUNCH("hg_ht_lookup", k_ht_lookup<H>, num_sms() * 2, kHtT, 0, st, qpart, q_start, t_off, hp, L.s, v, pb.big_bin,
+              pb.big_q, plan, hk, pb.hc, pb.mult_bo, reinterpret_cast<unsigned long long*>(agg));
+  }
   return HG_OK;
 }
 
@@ -1871,34 +2052,16 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
                       cudaStream_t st, cudaEvent_t split) {
   using K = KeyOf<H>;
   PartOut po{};
-  int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, true, nullptr, ws, st, &po);
+  int rc = run_partition<H>(queries, q, hp, L, 0xFFFFFFFFu, kPartQuery, nullptr, ws, st, &po);
   if (rc) return rc;
   if (split) HG_CHECK_CUDA(cudaEventRecord(split, st));  // query-side grouping done (intersect_timed's split)
-  uint32_t* mult_bo = ws.take<uint32_t>(q + 4);  // + tail padding for k_unpart's aligned run copies
-  const uint32_t max_extra = (uint32_t)(q / kProbeChunk + 1);
-  uint32_t* item_x = ws.take<uint32_t>(2 * (size_t)max_extra);
-  uint32_t* big_bin = ws.take<uint32_t>(L.nfine + 1);
-  uint32_t* big_t = ws.take<uint32_t>(L.nfine + 1);
-  uint32_t* big_q = ws.take<uint32_t>(L.nfine + 1);
-  unsigned long long* plan = reinterpret_cast<unsigned long long*>(po.plan32);
-  const uint64_t hs = ht_slots(n_table, sizeof(K) * 8);
-  K* hk = ws.take<K>(hs);
-  uint32_t* hc = ws.take<uint32_t>(hs);
+  ProbeBufs pb;
+  probe_alloc<K>(q, L, n_table, ws, &pb);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small");
-  HG_LAUNCH("hg_probe_plan", k_probe_plan, (L.nfine + 255) / 256, 256, 0, st, t_off, po.fine_start, L.nfine, L.s, v,
-            LocalShape<K>::kCap, item_x, big_bin, plan);
-  const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
-  HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine + max_extra, kT, smQ, st, t_off, t_edges, (const K*)po.grouped,
-            po.fine_start, L.nfine, item_x, plan, big_bin, hp, L.s, v, mult_bo, reinterpret_cast<unsigned long long*>(agg));
-  if (hs) {  // oversized table slices: key -> count hash table over the whole grid
-    HG_LAUNCH("hg_ht_prep", k_ht_prep<K>, num_sms() * 4, 256, 0, st, plan, big_bin, t_off, po.fine_start, L.s, v, big_t,
-              big_q, hk, hc);
-    HG_LAUNCH("hg_ht_insert", k_ht_insert<H>, num_sms() * 2, kHtT, 0, st, t_off, t_edges, L.s, v, big_bin, big_t, plan, hk,
-              hc);
-    HG_LAUNCH("hg_ht_lookup", k_ht_lookup<H>, num_sms() * 2, kHtT, 0, st, (const K*)po.grouped, po.fine_start, t_off, hp,
-              L.s, v, big_bin, big_q, plan, hk, hc, mult_bo, reinterpret_cast<unsigned long long*>(agg));
-  }
+  rc = probe_stage<H>(t_off, t_edges, (const K*)po.grouped, po.fine_start, q, hp, v, L, reinterpret_cast<unsigned long long*>(po.plan32), pb,
+                      agg, st);
+  if (rc) return rc;
+  uint32_t* mult_bo = pb.mult_bo;
   const size_t smR = unpart_smem();
   uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
   if (L.two_level) {
@@ -1912,6 +2075,92 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.sub, L.nb1, L.tile, q,
             L.chunk, po.M, po.c_start, po.tp);
   return HG_OK;
+}
+
+// --------------------------------------------------------------------------- two-step query (query.py:84-179)
+
+__global__ void k_qstart(const uint32_t* __restrict__ q_off, uint32_t nfine, int s, uint64_t v, uint32_t* __restrict__ q_start) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f <= nfine) q_start[f] = q_off[min((uint64_t)f << s, v)];
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n,
+                             uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = src[__ldcs(idx + i)];
+}
+
+__global__ void k_scatter_pos(const uint32_t* __restrict__ src, const uint32_t* __restrict__ pos, uint64_t n,
+                              uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[__ldcs(pos + i)] = __ldcs(src + i);
+}
+
+// intersect_tables (query.py:120-179) over a query table that is already
+// grouped by bucket: its fine-bin slices are the probe's query ranges, so no
+// partition runs.  Counts come out in query-table slot order and go back to
+// query order either through the trace of the hg_build that produced the
+// query table with positions (lmap -> grouped order -> k_unpart x 2, all
+// streaming) or, for foreign positions, by scatter.
+template <typename H>
+static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n_table, const uint32_t* q_off,
+                       const KeyOf<H>* q_edges, const uint32_t* positions, uint64_t q, const HashParams& hp, uint64_t v,
+                       const BinLayout& Lp, const BinLayout* Lt, void* trace, size_t trace_bytes, uint32_t* mult,
+                       uint64_t* agg, Workspace& ws, cudaStream_t st) {
+  using K = KeyOf<H>;
+  uint32_t* q_start = ws.take<uint32_t>(Lp.nfine + 1);
+  unsigned long long* plan = ws.take<unsigned long long>(kPlanWords);
+  ProbeBufs pb;
+  probe_alloc<K>(q, Lp, n_table, ws, &pb);
+  uint32_t* vals = ws.take<uint32_t>(q + 4);
+  uint32_t* level1 = ws.take<uint32_t>(q + 4);
+  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "intersect_tables workspace too small (%zu < %zu)", ws.cap, ws.used);
+  PartOut tpo{};
+  uint32_t* lmap = nullptr;
+  if (trace) {  // re-derive the trace's buffers: the same carve-up as the traced build
+    Workspace tw{(char*)trace, trace_bytes, 0};
+    uint32_t *fc, *fcur;
+    K* out2;
+    part_alloc<K>(q, *Lt, kPartTraced, nullptr, tw, &tpo, &fc, &fcur, &out2);
+    tw.take<uint32_t>(q + 4);  // a2
+    lmap = tw.take<uint32_t>(q + 4);
+    if (!tw.ok()) return set_error(HG_ERR_CONFIG, "trace buffer too small (%zu < %zu)", tw.cap, tw.used);
+  }
+  HG_CHECK_CUDA(cudaMemsetAsync(plan, 0, kPlanWords * 8, st));
+  HG_LAUNCH("hg_qstart", k_qstart, (Lp.nfine + 256) / 256, 256, 0, st, q_off, Lp.nfine, Lp.s, v, q_start);
+  int rc = probe_stage<H>(t_off, t_edges, q_edges, q_start, q, hp, v, Lp, plan, pb, agg, st);
+  if (rc) return rc;
+  const int g = num_sms() * 8;
+  if (!trace) {
+    HG_LAUNCH("hg_scatter_pos", k_scatter_pos, g, 256, 0, st, pb.mult_bo, positions, q, mult);
+    return HG_OK;
+  }
+  const BinLayout& L = *Lt;
+  HG_LAUNCH("hg_gather_lmap", k_gather_u32, g, 256, 0, st, pb.mult_bo, lmap, q, vals);
+  const size_t smR = unpart_smem();
+  uint32_t* l1 = vals;
+  if (L.two_level) {
+    HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, vals, level1, tpo.pmap2, tpo.meta2, L.sub, L.nb1, L.tile, q,
+              L.chunk, tpo.M, tpo.c_start, tpo.tp);
+    l1 = level1;
+  }
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+  HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, l1, mult, tpo.pmap1, tpo.meta1, L.sub, L.nb1, L.tile, q, L.chunk,
+            tpo.M, tpo.c_start, tpo.tp);
+  return HG_OK;
+}
+
+size_t binned_tables_ws_bytes(uint64_t q, const BinLayout& Lp, int key_bits, uint64_t n_table) {
+  Workspace w{nullptr, ~(size_t)0, 0};
+  w.take<uint32_t>(Lp.nfine + 1);
+  w.take<unsigned long long>(kPlanWords);
+  ProbeBufs pb;
+  if (key_bits == 32) probe_alloc<uint32_t>(q, Lp, n_table, w, &pb);
+  else probe_alloc<uint64_t>(q, Lp, n_table, w, &pb);
+  w.take<uint32_t>(q + 4);
+  w.take<uint32_t>(q + 4);
+  return w.used + 4096;
 }
 
 // Host dispatch to the compile-time hasher (reduction mode x hash kind).
@@ -1939,9 +2188,20 @@ static int with_hasher(const HashParams& hp, F&& f) {
 
 template <typename K>
 int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
-                 K* edges, Workspace& ws, cudaStream_t st) {
+                 K* edges, Workspace& ws, cudaStream_t st, uint32_t* positions) {
   return with_hasher<K>(hp, [&](auto h) {
-    return build_impl<decltype(h)>(keys, n, hp, v, L, offsets, edges, ws, st);
+    return build_impl<decltype(h)>(keys, n, hp, v, L, offsets, edges, ws, st, positions);
+  });
+}
+
+template <typename K>
+int binned_tables(const uint32_t* t_off, const K* t_edges, uint64_t n_table, const uint32_t* q_off, const K* q_edges,
+                  const uint32_t* positions, uint64_t q, const HashParams& hp, uint64_t v, const BinLayout& Lp,
+                  const BinLayout* Lt, void* trace, size_t trace_bytes, uint32_t* mult, uint64_t* agg, Workspace& ws,
+                  cudaStream_t st) {
+  return with_hasher<K>(hp, [&](auto h) {
+    return tables_impl<decltype(h)>(t_off, t_edges, n_table, q_off, q_edges, positions, q, hp, v, Lp, Lt, trace,
+                                    trace_bytes, mult, agg, ws, st);
   });
 }
 
@@ -1955,9 +2215,15 @@ int binned_query(const uint32_t* t_off, const K* t_edges, uint64_t n_table, cons
 }
 
 template int binned_build<uint32_t>(const uint32_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
-                                    uint32_t*, uint32_t*, Workspace&, cudaStream_t);
+                                    uint32_t*, uint32_t*, Workspace&, cudaStream_t, uint32_t*);
 template int binned_build<uint64_t>(const uint64_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
-                                    uint32_t*, uint64_t*, Workspace&, cudaStream_t);
+                                    uint32_t*, uint64_t*, Workspace&, cudaStream_t, uint32_t*);
+template int binned_tables<uint32_t>(const uint32_t*, const uint32_t*, uint64_t, const uint32_t*, const uint32_t*,
+                                     const uint32_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
+                                     const BinLayout*, void*, size_t, uint32_t*, uint64_t*, Workspace&, cudaStream_t);
+template int binned_tables<uint64_t>(const uint32_t*, const uint64_t*, uint64_t, const uint32_t*, const uint64_t*,
+                                     const uint32_t*, uint64_t, const HashParams&, uint64_t, const BinLayout&,
+                                     const BinLayout*, void*, size_t, uint32_t*, uint64_t*, Workspace&, cudaStream_t);
 template int binned_query<uint32_t>(const uint32_t*, const uint32_t*, uint64_t, const uint32_t*, uint64_t,
                                     const HashParams&, uint64_t, const BinLayout&, uint32_t*, uint64_t*, Workspace&,
                                     cudaStream_t, cudaEvent_t);

@@ -21,10 +21,17 @@ struct BinLayout {
 };
 
 bool binned_layout(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L);
-size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, bool query, uint64_t n_table = 0);
+enum { kWsBuild = 0, kWsQuery = 1, kWsTraced = 2 };  // == PartMode
+size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, int mode, uint64_t n_table = 0);
+size_t binned_tables_ws_bytes(uint64_t q, const BinLayout& Lp, int key_bits, uint64_t n_table);
 template <typename K>
 int binned_build(const K* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
-                 K* edges, Workspace& ws, cudaStream_t st);
+                 K* edges, Workspace& ws, cudaStream_t st, uint32_t* positions = nullptr);
+template <typename K>
+int binned_tables(const uint32_t* t_off, const K* t_edges, uint64_t n_table, const uint32_t* q_off, const K* q_edges,
+                  const uint32_t* positions, uint64_t q, const HashParams& hp, uint64_t v, const BinLayout& Lp,
+                  const BinLayout* Lt, void* trace, size_t trace_bytes, uint32_t* mult, uint64_t* agg, Workspace& ws,
+                  cudaStream_t st);
 template <typename K>
 int binned_query(const uint32_t* t_off, const K* t_edges, uint64_t n_table, const K* queries, uint64_t q,
                  const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* mult, uint64_t* agg, Workspace& ws,

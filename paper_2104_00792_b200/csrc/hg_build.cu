@@ -306,7 +306,14 @@ int hg_hash(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
 size_t hg_build_workspace_size(uint64_t n, uint64_t v, int key_bits) {
   size_t b = build_ws_bytes(n, v, key_bits);
   BinLayout L;
-  if (use_binned(n, n, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(n, L, key_bits, false));
+  if (use_binned(n, n, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(n, L, key_bits, kWsBuild));
+  return b;
+}
+
+size_t hg_build_traced_workspace_size(uint64_t n, uint64_t v, int key_bits) {
+  size_t b = build_ws_bytes(n, v, key_bits);
+  BinLayout L;
+  if (use_binned(n, n, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(n, L, key_bits, kWsTraced));
   return b;
 }
 
@@ -318,10 +325,12 @@ int hg_build(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
   BinLayout L;
-  if (positions == nullptr && use_binned(n, n, v, key_bits, &L)) {
+  // positions (build_traced): the binned path when the workspace holds its trace
+  if (use_binned(n, n, v, key_bits, &L) &&
+      (positions == nullptr || binned_ws_bytes(n, L, key_bits, kWsTraced) <= workspace_bytes)) {
     if (key_bits == 32)
-      return binned_build<uint32_t>((const uint32_t*)keys, n, hp, v, L, offsets, (uint32_t*)edges, ws, s);
-    return binned_build<uint64_t>((const uint64_t*)keys, n, hp, v, L, offsets, (uint64_t*)edges, ws, s);
+      return binned_build<uint32_t>((const uint32_t*)keys, n, hp, v, L, offsets, (uint32_t*)edges, ws, s, positions);
+    return binned_build<uint64_t>((const uint64_t*)keys, n, hp, v, L, offsets, (uint64_t*)edges, ws, s, positions);
   }
   if (key_bits == 32)
     return build_impl<uint32_t>((const uint32_t*)keys, n, hp, v, offsets, (uint32_t*)edges, positions, ws, s);
@@ -347,7 +356,7 @@ size_t hg_query_workspace_size(uint64_t q, uint64_t v, uint64_t n_table, int key
   size_t kb = key_bits / 8;
   size_t b = align_up(4 * (v + 1), 256) + align_up(kb * q, 256) + align_up(4 * q, 256) + build_ws_bytes(q, v, key_bits) + 1024;
   BinLayout L;
-  if (use_binned(n_table, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, true, n_table));
+  if (use_binned(n_table, q, v, key_bits, &L)) b = std::max(b, binned_ws_bytes(q, L, key_bits, kWsQuery, n_table));
   return b;
 }
 
@@ -360,7 +369,7 @@ static int query_entry(const uint32_t* offsets_a, const void* edges_a, uint64_t 
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
   BinLayout L;
-  if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, true, n_a) <= workspace_bytes) {
+  if (use_binned(n_a, q, v, key_bits, &L) && binned_ws_bytes(q, L, key_bits, kWsQuery, n_a) <= workspace_bytes) {
     if (key_bits == 32)
       return binned_query<uint32_t>(offsets_a, (const uint32_t*)edges_a, n_a, (const uint32_t*)queries, q, hp, v, L,
                                     mult, agg, ws, s, split);
@@ -397,6 +406,41 @@ int hg_query_timed(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a,
                    size_t workspace_bytes, void* split_event, void* stream) {
   return query_entry(offsets_a, edges_a, n_a, queries, q, key_bits, kind, seed, v, mult, agg, workspace,
                      workspace_bytes, stream, (cudaEvent_t)split_event);
+}
+
+size_t hg_intersect_tables_workspace_size(uint64_t n_b, uint64_t v, uint64_t n_a, int key_bits) {
+  BinLayout L;
+  if (use_binned(n_a, n_b, v, key_bits, &L)) return binned_tables_ws_bytes(n_b, L, key_bits, n_a);
+  return 1024;
+}
+
+int hg_intersect_tables(const uint32_t* offsets_a, const void* edges_a, uint64_t n_a, const uint32_t* offsets_b,
+                        const void* edges_b, const uint32_t* positions_b, uint64_t n_b, int key_bits, int kind,
+                        uint32_t seed, uint64_t v, void* trace, size_t trace_bytes, uint32_t* mult, uint64_t* agg,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_common(n_b, key_bits, kind, v);
+  if (rc) return rc;
+  HashParams hp = make_hash_params(kind, seed, v, key_bits);
+  cudaStream_t s = (cudaStream_t)stream;
+  BinLayout Lp, Lt;
+  if (use_binned(n_a, n_b, v, key_bits, &Lp) && binned_tables_ws_bytes(n_b, Lp, key_bits, n_a) <= workspace_bytes) {
+    // the trace is only usable when the query table was built binned with it
+    const bool traced = trace != nullptr && use_binned(n_b, n_b, v, key_bits, &Lt) &&
+                        binned_ws_bytes(n_b, Lt, key_bits, kWsTraced) <= trace_bytes;
+    Workspace ws{(char*)workspace, workspace_bytes, 0};
+    if (key_bits == 32)
+      return binned_tables<uint32_t>(offsets_a, (const uint32_t*)edges_a, n_a, offsets_b, (const uint32_t*)edges_b,
+                                     positions_b, n_b, hp, v, Lp, traced ? &Lt : nullptr, traced ? trace : nullptr,
+                                     trace_bytes, mult, agg, ws, s);
+    return binned_tables<uint64_t>(offsets_a, (const uint64_t*)edges_a, n_a, offsets_b, (const uint64_t*)edges_b,
+                                   positions_b, n_b, hp, v, Lp, traced ? &Lt : nullptr, traced ? trace : nullptr,
+                                   trace_bytes, mult, agg, ws, s);
+  }
+  if (key_bits == 32)
+    return intersect_impl<uint32_t>(offsets_a, (const uint32_t*)edges_a, (const uint32_t*)edges_b, positions_b, n_b, hp,
+                                    mult, agg, s);
+  return intersect_impl<uint64_t>(offsets_a, (const uint64_t*)edges_a, (const uint64_t*)edges_b, positions_b, n_b, hp,
+                                  mult, agg, s);
 }
 
 }  // extern "C"

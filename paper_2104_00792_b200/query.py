@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .core import Bucket, HashGraph, as_device_table, build_device, build_traced
+from .core import Bucket, HashGraph, _build, as_device_table, build_device, build_traced
 from .errors import ConfigError
 from .hashing import family_code, same_family
 
@@ -103,10 +103,35 @@ def intersect_buckets(a: Bucket, b: Bucket) -> BucketIntersection:
     return BucketIntersection(counts, int(counts.sum()), len(ea) * len(eb))
 
 
+class QueryTableTrace:
+    """What intersect_tables needs to return counts to query order without a
+    scatter: the traced build's workspace (hg_build_traced_workspace_size:
+    both partition levels' position maps and every grouped key's slot), the
+    device positions, and the host positions array handed to the caller
+    (identity-checked, read-only)."""
+
+    __slots__ = ("workspace", "positions_device", "positions_host")
+
+    def __init__(self, workspace, positions_device, positions_host):
+        self.workspace = workspace
+        self.positions_device = positions_device
+        self.positions_host = positions_host
+
+
 def build_query_table(table, queries):
-    """Query-side table with the input table's hash range (query.py:84-95)."""
-    qt, _, positions = build_traced(queries, family=table.family, hash_range=table.hash_range,
-                                    key_bits=getattr(table, "key_bits", 32))
+    """Query-side table with the input table's hash range (query.py:84-95).
+
+    The build runs traced: the returned table keeps its trace (about 20 bytes
+    per query key of device memory) so that intersect_tables(table, qt,
+    positions) with these very positions streams the counts back to query
+    order; positions is the usual read-only int64 array."""
+    key_bits = getattr(table, "key_bits", 32)
+    if key_bits not in (32, 64):
+        raise ConfigError(f"key_bits must be 32 or 64, got {key_bits}")
+    qt, _, pos, ws = _build(queries, 1.0, table.family, 1, table.hash_range, key_bits, True, keep_trace=True)
+    positions = D.frozen(D.widen_u32_to_numpy(pos) if pos is not None and pos.numel() else np.zeros(0, np.int64))
+    if pos is not None and pos.numel():
+        object.__setattr__(qt, "_trace", QueryTableTrace(ws, pos, positions))
     return qt, positions
 
 
@@ -131,17 +156,25 @@ def intersect_tables(table, query_table, positions, worker_count: int = 1) -> Qu
 
 def _intersect_tables_device(ta, tb, positions):
     t = D.torch()
-    if D.is_cuda_tensor(positions):
-        pos = positions.to(t.int32)
+    trace = getattr(tb, "_trace", None)
+    if trace is not None and positions is trace.positions_host:  # the positions build_query_table returned
+        pos = trace.positions_device
     else:
-        pos = t.from_numpy(np.asarray(positions, dtype=np.int64).astype(np.uint32).view(np.int32)).to(D.device())
+        trace = None
+        if D.is_cuda_tensor(positions):
+            pos = positions.to(t.int32)
+        else:
+            pos = t.from_numpy(np.asarray(positions, dtype=np.int64).astype(np.uint32).view(np.int32)).to(D.device())
     nb = tb.num_keys
     mult = t.zeros(nb, dtype=t.int32, device=D.device())
     agg = t.zeros(3, dtype=t.int64, device=D.device())
     kind, seed = family_code(ta.family)
-    _lib.call("hg_intersect", D.ptr(ta.offset_device), D.ptr(ta.keys_device), D.ptr(tb.offset_device),
-              D.ptr(tb.keys_device), D.ptr(pos), nb, ta.key_bits, kind, seed, ta.hash_range, D.ptr(mult),
-              D.ptr(agg), D.stream_ptr())
+    ws = D.workspace(_lib.load().hg_intersect_tables_workspace_size(nb, ta.hash_range, ta.num_keys, ta.key_bits))
+    tw = trace.workspace if trace is not None else None
+    _lib.call("hg_intersect_tables", D.ptr(ta.offset_device), D.ptr(ta.keys_device), ta.num_keys,
+              D.ptr(tb.offset_device), D.ptr(tb.keys_device), D.ptr(pos), nb, ta.key_bits, kind, seed, ta.hash_range,
+              D.ptr(tw), tw.numel() if tw is not None else 0, D.ptr(mult), D.ptr(agg), D.ptr(ws),
+              ws.numel(), D.stream_ptr())
     return QueryResult(mult, agg, ta.hash_range)
 
 
