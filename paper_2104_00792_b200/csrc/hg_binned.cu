@@ -940,35 +940,34 @@ k_unpart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
 // Forward of a partition level for per-key uint32 values (the inverse of
 // k_unpart): each tile's values (input order; level 1 with vals == nullptr:
 // the input index itself) go to their staged slots through the recorded u16
-// position map, then every run leaves for its recorded destination -- the
-// same permutation k_part1 / k_part2 applied to the keys, with no hashing or
-// ranking.  build_traced uses it to carry input indices to the grouped order.
+// position map -- the staging layout k_part1 / k_part2 used for the keys, so
+// every run's aligned body leaves with one TMA bulk store -- with no hashing
+// or ranking.  build_traced uses it to carry input indices to the grouped
+// order.  The next tile's map, values and metadata load during this tile's
+// stores.
 template <int kLevel>
 __global__ void __launch_bounds__(kT, 2)
 k_repart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const uint16_t* __restrict__ pmap,
          const uint32_t* __restrict__ meta, uint32_t sub, uint32_t nb, uint32_t tile, uint64_t n, uint64_t chunk,
          const uint32_t* __restrict__ M, const uint32_t* __restrict__ c_start, const uint32_t* __restrict__ tp_g) {
+  constexpr int VPT = 8192 / kT;  // values per thread (tile <= 8192)
   extern __shared__ __align__(128) unsigned char s_raw[];
   uint32_t* staged = reinterpret_cast<uint32_t*>(s_raw);  // kUnpStaged
   __shared__ uint32_t toff[kMaxBins + 1], base[kMaxBins], tps[kMaxBins + 1];
   const uint32_t nbb = kLevel == 1 ? nb : sub;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t lo = 0, hi = 0;
   uint32_t ntiles;
   if (kLevel == 1) {
     lo = (uint64_t)blockIdx.x * chunk;
     hi = min(n, lo + chunk);
     ntiles = hi > lo ? (uint32_t)((hi - lo + tile - 1) / tile) : 0u;
-    for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) base[x] = c_start[x] + M[(uint64_t)blockIdx.x * nb + x];
   } else {
     for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) tps[i] = tp_g[i];
     __syncthreads();
     const uint32_t tot = tps[nb];
     ntiles = tot > blockIdx.x ? (tot - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
   }
-  for (uint32_t it = 0; it < ntiles; it++) {
-    uint64_t t0, tix;
-    uint32_t m;
+  auto tile_of = [&](uint32_t it, uint64_t& t0, uint32_t& m, uint64_t& tix) {
     if (kLevel == 1) {
       t0 = lo + (uint64_t)it * tile;
       m = (uint32_t)min((uint64_t)tile, hi - t0);
@@ -984,27 +983,63 @@ k_repart(const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, const ui
       m = min(tile, c_start[a + 1] - (uint32_t)t0);
       tix = t;
     }
-    for (uint32_t x = threadIdx.x; x <= nbb; x += blockDim.x) {
-      if (kLevel == 1) {
-        toff[x] = meta[tix * (nb + 1) + x];
-      } else {
-        toff[x] = meta[tix * (2 * sub + 1) + sub + x];
-        if (x < sub) base[x] = meta[tix * (2 * sub + 1) + x];
+  };
+  // per-thread registers of a tile: its map slots, values and (threads <= nbb) meta words
+  uint32_t pm[VPT], vv[VPT], r0 = 0, r1 = 0;
+  uint64_t t0 = 0, tix = 0;
+  uint32_t m = 0;
+  auto load = [&](uint32_t it) {
+    tile_of(it, t0, m, tix);
+#pragma unroll
+    for (int k = 0; k < VPT; k++) {
+      const uint32_t i = k * kT + threadIdx.x;
+      pm[k] = i < m ? (uint32_t)pmap[t0 + i] : 0u;
+      vv[k] = i < m ? (vals ? vals[t0 + i] : (uint32_t)(t0 + i)) : 0u;
+    }
+    const uint32_t x = threadIdx.x;
+    if (kLevel == 1) {
+      if (x <= nb) r0 = meta[tix * (nb + 1) + x];
+    } else {
+      if (x <= sub) r0 = meta[tix * (2 * sub + 1) + sub + x];
+      if (x < sub) r1 = meta[tix * (2 * sub + 1) + x];
+    }
+  };
+  if (ntiles) load(0);
+  for (uint32_t it = 0; it < ntiles; it++) {
+    const uint32_t mc = m;
+    if (threadIdx.x < nbb) tma_store_wait_read();  // the previous tile's runs have left staged
+    __syncthreads();
+    const uint32_t x = threadIdx.x;
+    if (kLevel == 1) {
+      if (x < nb) base[x] = it == 0 ? c_start[x] + M[(uint64_t)blockIdx.x * nb + x] : base[x] + toff[x + 1] - toff[x];
+    } else if (x < sub) {
+      base[x] = r1;
+    }
+    __syncthreads();  // (level 1: base chained from the previous tile's toff before toff is replaced)
+    if (x <= nbb) toff[x] = r0;
+#pragma unroll
+    for (int k = 0; k < VPT; k++)
+      if (k * kT + threadIdx.x < mc) staged[pm[k]] = vv[k];
+    fence_proxy_async();  // staged (generic writes) -> TMA bulk-store reads
+    __syncthreads();
+    if (it + 1 < ntiles) load(it + 1);  // next tile's loads fly during the stores
+    if (threadIdx.x < nbb) {
+      const uint32_t b = threadIdx.x;
+      const uint32_t c0 = toff[b], cnt = toff[b + 1] - c0, g = base[b];
+      if (cnt) {
+        const uint32_t p = pad_start(c0, b, g);
+        const uint32_t h = min(cnt, (kPadMod - (g & (kPadMod - 1))) & (kPadMod - 1));
+        const uint32_t body = (cnt - h) & ~(kPadMod - 1);
+        for (uint32_t i = 0; i < h; i++) out[g + i] = staged[p + i];
+        if (body) {
+          tma_store_1d(out + g + h, staged + p + h, body * 4u);
+          tma_store_commit();
+        }
+        for (uint32_t i = h + body; i < cnt; i++) out[g + i] = staged[p + i];
       }
     }
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
-      staged[pmap[t0 + i]] = vals ? vals[t0 + i] : (uint32_t)(t0 + i);
-    __syncthreads();
-    for (uint32_t b = warp; b < nbb; b += kT / 32) {  // one warp per run: coalesced stores
-      const uint32_t c0 = toff[b], cnt = toff[b + 1] - c0, d = base[b];
-      const uint32_t p = pad_start(c0, b, d);
-      for (uint32_t k = lane; k < cnt; k += 32) out[d + k] = staged[p + k];
-    }
-    __syncthreads();
-    if (kLevel == 1)
-      for (uint32_t x = threadIdx.x; x < nb; x += blockDim.x) base[x] += toff[x + 1] - toff[x];
-    __syncthreads();
   }
+  if (threadIdx.x < nbb) tma_store_wait_all();
 }
 
 // --------------------------------------------------------------------------- C: local build
@@ -1229,10 +1264,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
         rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
       }
       stg[rel] = key;
-      if (kTrace) {
-        positions[lo + rel] = a2[g];
-        lmap[g] = lo + rel;
-      }
+      if (kTrace) lmap[g] = lo + rel;
     };
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
@@ -1263,6 +1295,47 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       if (gh < g0) edges[gh] = staged[gh - lo_al];
       const uint32_t gt = g1 + threadIdx.x;
       if (gt < hi) edges[gt] = staged[gt - lo_al];
+    }
+    if (kTrace) {
+      // positions through the same staging buffer once the edges have left
+      // it: slot rel of the bin gets a2[g] of the key placed there, then one
+      // bulk store (u32 view, 16-byte congruent to positions + lo)
+      if (threadIdx.x == 0) tma_store_wait_read();
+      __syncthreads();
+      uint32_t* st32 = reinterpret_cast<uint32_t*>(staged) + (lo & 3u);
+      auto place_pos = [&](K key, int k, uint32_t g) {
+        uint32_t rel;
+        if (kRehash) {
+          const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
+          rel = get16(c16, l) + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
+        } else {
+          rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
+        }
+        st32[rel] = a2[g];
+      };
+#pragma unroll
+      for (int i = 0; i < CPT; i++) {
+        const uint32_t c = i * NT + threadIdx.x;
+        const uint32_t e0 = c * VPL;
+        if (c < nch) {
+#pragma unroll
+          for (int j = 0; j < (int)VPL; j++)
+            if (e0 + j - sh < cnt) place_pos(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      const uint32_t p0 = min(hi, (lo + 3) & ~3u), p1 = max(p0, hi & ~3u);
+      if (threadIdx.x == 0 && p1 > p0) {
+        tma_store_1d(positions + p0, st32 + (p0 - lo), (p1 - p0) * 4u);
+        tma_store_commit();
+      }
+      if (threadIdx.x < 4) {
+        const uint32_t gh = lo + threadIdx.x;
+        if (gh < p0) positions[gh] = st32[gh - lo];
+        const uint32_t gt = p1 + threadIdx.x;
+        if (gt < hi) positions[gt] = st32[gt - lo];
+      }
     }
     f = fn;
   }
@@ -2090,6 +2163,27 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
     out[i] = src[__ldcs(idx + i)];
 }
 
+// Counts in query-table slot order -> grouped order, one CTA per fine bin of
+// the trace's layout: a bin's slots and its grouped keys share the range
+// [fine_start[f], fine_start[f+1]), so the bin's counts are staged in smem and
+// read back through lmap (coalesced in and out); bins above the smem
+// capacity gather from global memory.
+constexpr uint32_t kPermCap = 20480;
+
+__global__ void __launch_bounds__(512) k_perm_bins(const uint32_t* __restrict__ src, const uint32_t* __restrict__ lmap,
+                                                   const uint32_t* __restrict__ fine_start, uint32_t* __restrict__ out) {
+  __shared__ uint32_t sm[kPermCap];
+  const uint32_t f = blockIdx.x;
+  const uint32_t lo = fine_start[f], hi = fine_start[f + 1], cnt = hi - lo;
+  if (cnt <= kPermCap) {
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = __ldcs(src + lo + i);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[lo + i] = sm[__ldcs(lmap + lo + i) - lo];
+  } else {
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[lo + i] = src[lmap[lo + i]];
+  }
+}
+
 __global__ void k_scatter_pos(const uint32_t* __restrict__ src, const uint32_t* __restrict__ pos, uint64_t n,
                               uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -2136,7 +2230,7 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
     return HG_OK;
   }
   const BinLayout& L = *Lt;
-  HG_LAUNCH("hg_gather_lmap", k_gather_u32, g, 256, 0, st, pb.mult_bo, lmap, q, vals);
+  HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, 0, st, pb.mult_bo, lmap, tpo.fine_start, vals);
   const size_t smR = unpart_smem();
   uint32_t* l1 = vals;
   if (L.two_level) {

@@ -63,3 +63,16 @@ ok2 = torch.equal(mult, r.multiplicities_device)
 print(json.dumps({"log2": L, "intersect_ms": round(t_fused, 3), "build_query_table_ms": round(t_bqt, 3),
                   "intersect_tables_traced_ms": round(t_it, 3), "intersect_tables_scatter_ms": round(t_sc, 3),
                   "two_step_over_fused": round((t_bqt + t_it) / t_fused, 2), "exact": bool(ok and ok2)}))
+
+# per-kernel device times of one two-step run (library-recorded CUDA events)
+_lib.timing_enable(True)
+_lib.timing_collect()
+bqt()
+tables(trace)
+torch.cuda.synchronize()
+from collections import defaultdict  # noqa: E402
+acc = defaultdict(float)
+for name, ms in _lib.timing_collect(1 << 14):
+    acc[name] += ms
+_lib.timing_enable(False)
+print(" ".join(f"{k} {v:.3f}" for k, v in sorted(acc.items(), key=lambda kv: -kv[1])))
