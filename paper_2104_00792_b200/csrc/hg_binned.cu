@@ -2172,7 +2172,7 @@ constexpr uint32_t kPermCap = 20480;
 
 __global__ void __launch_bounds__(512) k_perm_bins(const uint32_t* __restrict__ src, const uint32_t* __restrict__ lmap,
                                                    const uint32_t* __restrict__ fine_start, uint32_t* __restrict__ out) {
-  __shared__ uint32_t sm[kPermCap];
+  extern __shared__ uint32_t sm[];  // kPermCap
   const uint32_t f = blockIdx.x;
   const uint32_t lo = fine_start[f], hi = fine_start[f + 1], cnt = hi - lo;
   if (cnt <= kPermCap) {
@@ -2230,7 +2230,8 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
     return HG_OK;
   }
   const BinLayout& L = *Lt;
-  HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, 0, st, pb.mult_bo, lmap, tpo.fine_start, vals);
+  HG_CHECK_CUDA(cudaFuncSetAttribute(k_perm_bins, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kPermCap * 4)));
+  HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, kPermCap * 4, st, pb.mult_bo, lmap, tpo.fine_start, vals);
   const size_t smR = unpart_smem();
   uint32_t* l1 = vals;
   if (L.two_level) {
