@@ -2173,12 +2173,28 @@ constexpr uint32_t kPermCap = 20480;
 __global__ void __launch_bounds__(512) k_perm_bins(const uint32_t* __restrict__ src, const uint32_t* __restrict__ lmap,
                                                    const uint32_t* __restrict__ fine_start, uint32_t* __restrict__ out) {
   extern __shared__ uint32_t sm[];  // kPermCap
+  constexpr int U = 8;  // elements per thread per round, loads first
   const uint32_t f = blockIdx.x;
   const uint32_t lo = fine_start[f], hi = fine_start[f + 1], cnt = hi - lo;
+  const uint32_t step = U * blockDim.x;
   if (cnt <= kPermCap) {
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = __ldcs(src + lo + i);
+    for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += step) {
+      uint32_t x[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) x[u] = i0 + u * blockDim.x < cnt ? __ldcs(src + lo + i0 + u * blockDim.x) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (i0 + u * blockDim.x < cnt) sm[i0 + u * blockDim.x] = x[u];
+    }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[lo + i] = sm[__ldcs(lmap + lo + i) - lo];
+    for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += step) {
+      uint32_t x[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) x[u] = i0 + u * blockDim.x < cnt ? __ldcs(lmap + lo + i0 + u * blockDim.x) - lo : 0u;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (i0 + u * blockDim.x < cnt) out[lo + i0 + u * blockDim.x] = sm[x[u]];
+    }
   } else {
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[lo + i] = src[lmap[lo + i]];
   }
