@@ -17,7 +17,10 @@ LABEL = {  # kernel function -> launch label used by the library / bench
     "k_hist": "hg_hist", "k_colscan": "hg_colscan", "k_starts": "hg_starts", "k_local_build_big": "hg_local_build_big",
     "k_local_build": "hg_local_build", "k_local_build_p": "hg_local_build", "k_local_probe": "hg_local_probe", "k_unpart<2>": "hg_unpart2",
     "k_unpart<1>": "hg_unpart1", "k_count": "hg_count", "k_scan": "hg_scan", "k_place": "hg_place",
-    "k_intersect": "hg_intersect", "k_generate32": "hg_generate",
+    "k_intersect": "hg_intersect", "k_generate32": "hg_generate", "k_probe_plan": "hg_probe_plan",
+    "k_big_count": "hg_big_count", "k_big_place": "hg_big_place", "k_ht_prep": "hg_ht_prep",
+    "k_ht_insert": "hg_ht_insert", "k_ht_lookup": "hg_ht_lookup", "k_qstart": "hg_qstart",
+    "k_perm_bins": "hg_perm_bins", "k_scatter_pos": "hg_scatter_pos",
 }
 
 
@@ -25,10 +28,11 @@ def label(fn: str) -> str:
     name = fn.split("(")[0].replace("void ", "").replace("hg::", "").strip()
     base = name.split("<")[0]
     if base in ("k_part1", "k_part2"):
-        q = name.rstrip(">").endswith("1") or ", true" in name
+        targs = [t.strip() for t in name[name.index(">") + 1:].strip(" ,>").split(",")] if ">" in name else []
+        q = ", true" in name or (len(targs) >= 1 and targs[0] == "1")
         return f"hg_{base[2:]}" + ("_q" if q else "")
-    if base == "k_unpart":
-        return "hg_unpart2" if "<2>" in name else "hg_unpart1"
+    if base in ("k_unpart", "k_repart"):
+        return f"hg_{base[2:]}" + ("2" if "<2>" in name else "1")
     return LABEL.get(base, name)
 
 
