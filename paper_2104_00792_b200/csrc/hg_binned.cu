@@ -466,6 +466,7 @@ struct PartSmem {
   uint32_t pt[kMaxBins];        // padded staged start per bin
   uint32_t dst[kMaxBins];       // global write base per bin
   uint32_t tp[kMaxBins + 1];    // level-2 tile prefix (P2 only)
+  uint32_t cs[kMaxBins + 1];    // level-1 bin starts (P2 only): locating a tile needs no global load
   alignas(8) uint64_t bar;  // TMA load barrier
 };
 
@@ -691,7 +692,10 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
   constexpr uint32_t VPL = 16 / sizeof(K);
   extern __shared__ __align__(128) unsigned char s_raw[];
   PartSmem<K>& s = *reinterpret_cast<PartSmem<K>*>(s_raw);
-  for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) s.tp[i] = tp_g[i];
+  for (uint32_t i = threadIdx.x; i <= nb1; i += blockDim.x) {
+    s.tp[i] = tp_g[i];
+    s.cs[i] = c_start[i];
+  }
   if (threadIdx.x == 0) {
     mbar_init(&s.bar, 1);
     fence_proxy_async();
@@ -710,8 +714,8 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
       const uint32_t mid = (a + z) >> 1;
       if (s.tp[mid] <= t) a = mid; else z = mid;
     }
-    const uint32_t t0 = c_start[a] + (t - s.tp[a]) * TS::kTile;
-    const uint32_t m = min((uint32_t)TS::kTile, c_start[a + 1] - t0);
+    const uint32_t t0 = s.cs[a] + (t - s.tp[a]) * TS::kTile;
+    const uint32_t m = min((uint32_t)TS::kTile, s.cs[a + 1] - t0);
     s_loc[0] = a;
     s_loc[1] = t0;
     s_loc[2] = m;
