@@ -3,7 +3,10 @@ computation is a libhashgraph_b200 kernel launched through _lib."""
 
 from __future__ import annotations
 
+import os
+import threading
 import warnings
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -119,23 +122,107 @@ def to_device_keys(keys, key_bits: int = 32):
             keys = keys.to(want)
         return keys.to(device(), non_blocking=keys.is_pinned())
     arr = coerce_host_keys(keys, key_bits)
+    return h2d_numpy(arr.view(np.int32 if key_bits == 32 else np.int64))
+
+
+# ---- host <-> device transfers for numpy callers (the reference API's arrays)
+#
+# A pageable copy runs at ~10 GB/s and a fresh pageable destination pays a
+# page fault per 4 KB (a 2 GB int64 result took ~1 s).  Host -> device goes
+# through two cached pinned chunks filled by a thread pool (several cores'
+# memory bandwidth) while the other chunk's DMA runs; device -> host lands in
+# pinned memory from torch's caching host allocator and is returned as a
+# numpy view of it (no copy, no page faults once the allocator has the block).
+_H2D_CHUNK = 64 << 20  # bytes per staging chunk
+_state = threading.local()
+_pool = None
+_pool_lock = threading.Lock()
+
+
+def _copy_pool():
+    global _pool
+    with _pool_lock:
+        if _pool is None:
+            _pool = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)))
+    return _pool
+
+
+def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src with the copy split over the pool (numpy releases the GIL)."""
+    n = len(src)
+    parts = 8 if n * src.itemsize >= (8 << 20) else 1
+    if parts == 1:
+        np.copyto(dst, src)
+        return
+    step = -(-n // parts)
+    futs = [_copy_pool().submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
+def _staging():
+    t = torch()
+    key = t.cuda.current_device()
+    st = getattr(_state, "staging", None)
+    if st is None or st[0] != key:
+        bufs = [t.empty(_H2D_CHUNK, dtype=t.uint8, pin_memory=True) for _ in range(2)]
+        evs = [t.cuda.Event() for _ in range(2)]
+        st = (key, bufs, evs, [False, False])
+        _state.staging = st
+    return st
+
+
+def h2d_numpy(arr: np.ndarray):
+    """Contiguous numpy array -> CUDA tensor of the same dtype, enqueued on the
+    current stream through the pinned staging chunks (returns after the last
+    chunk is staged; the DMA itself is asynchronous)."""
+    t = torch()
+    arr = np.ascontiguousarray(arr)
     with warnings.catch_warnings():  # read-only arrays (e.g. a table's keys) are only read here
         warnings.simplefilter("ignore", UserWarning)
-        host = t.from_numpy(arr.view(np.int32 if key_bits == 32 else np.int64))
-    return host.to(device(), non_blocking=False)
+        src = t.from_numpy(arr)
+    out = t.empty(arr.shape, dtype=src.dtype, device=device())
+    nbytes = arr.nbytes
+    if nbytes < (1 << 20):
+        return src.to(device())
+    _, bufs, evs, used = _staging()
+    flat = arr.view(np.uint8).reshape(-1)
+    out_b = out.view(t.uint8).reshape(-1)
+    stream = t.cuda.current_stream()
+    for i, off in enumerate(range(0, nbytes, _H2D_CHUNK)):
+        k = i & 1
+        m = min(_H2D_CHUNK, nbytes - off)
+        if used[k]:
+            evs[k].synchronize()  # the chunk's previous DMA has read it
+        _par_copy(bufs[k].numpy()[:m], flat[off:off + m])
+        out_b[off:off + m].copy_(bufs[k][:m], non_blocking=True)
+        evs[k].record(stream)
+        used[k] = True
+    return out
+
+
+def d2h_numpy(t_dev) -> np.ndarray:
+    """CUDA tensor -> numpy array viewing pinned host memory (synchronises)."""
+    t = torch()
+    host = t.empty(t_dev.shape, dtype=t_dev.dtype, pin_memory=True)
+    host.copy_(t_dev, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    return host.numpy()
 
 
 def to_numpy_keys(t, key_bits: int = 32) -> np.ndarray:
-    a = t.cpu().numpy()
+    with on(t):
+        a = d2h_numpy(t)
     return a.view(np_key_dtype(key_bits))
 
 
 def widen_u32_to_numpy(t) -> np.ndarray:
     """uint32 device array -> int64 numpy (kernel widening, then one D2H)."""
     n = t.numel()
-    out = torch().empty(n, dtype=torch().int64, device=t.device)
-    _lib.call("hg_widen_u32", ptr(t), n, ptr(out), stream_ptr())
-    return out.cpu().numpy()
+    with on(t):
+        out = torch().empty(n, dtype=torch().int64, device=t.device)
+        _lib.call("hg_widen_u32", ptr(t), n, ptr(out), stream_ptr())
+        return d2h_numpy(out)
 
 
 def frozen(a: np.ndarray) -> np.ndarray:
