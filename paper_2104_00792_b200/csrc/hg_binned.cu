@@ -1992,12 +1992,12 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   HG_CHECK_CUDA(cudaMemsetAsync(fine_cnt, 0, 4 * (size_t)L.nfine, st));
   if (L.nfine <= kHistMax) {
     const size_t smA = (size_t)L.nfine * 4;
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+    HG_SET_SMEM((k_hist<H, false>), (int)smA);
     HG_LAUNCH("hg_hist", (k_hist<H, false>), L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk,
               po->M, fine_cnt, 0u, L.nfine);
   } else {  // more fine bins than one smem histogram holds: one pass per range
     const size_t smA = (size_t)kHistMax * 4;
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_hist<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+    HG_SET_SMEM((k_hist<H, true>), (int)smA);
     for (uint32_t f_lo = 0; f_lo < L.nfine; f_lo += kHistMax)
       HG_LAUNCH("hg_hist", (k_hist<H, true>), L.grid, kT, smA, st, keys, n, hp, L.s, L.nfine, L.group, L.nb1, L.chunk,
                 po->M, fine_cnt, f_lo, std::min<uint32_t>(kHistMax, L.nfine - f_lo));
@@ -2005,23 +2005,23 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
   HG_LAUNCH("hg_colscan", k_colscan, L.nb1, (L.grid + 31) / 32 * 32 > 1024 ? 1024 : (L.grid + 31) / 32 * 32,
             (size_t)L.grid * 4, st, po->M, L.grid, L.nb1);
   const size_t smS = (size_t)std::min<uint32_t>(L.nfine, kStartsChunk) * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_starts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smS));
+  HG_SET_SMEM((k_starts), (int)smS);
   HG_LAUNCH("hg_starts", k_starts, 1, 1024, smS, st, fine_cnt, L.nfine, L.group, L.nb1, L.tile, cap, po->fine_start,
             po->c_start, po->tp, fine_cursor, po->big_list, po->big_count, (uint32_t)BigShape<K>::kChunk, po->big_cp,
             po->big_done, po->plan32, po->plan32 ? (uint32_t)(2 * kPlanWords) : 0u);
   const size_t smP = part_smem(sizeof(K) * 8);
   if (query) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_SET_SMEM((k_part1<H, true>), (int)smP);
     HG_LAUNCH("hg_part1_q", (k_part1<H, true>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
               po->M, po->c_start, out1, po->pmap1, po->meta1);
   } else {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_part1<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    HG_SET_SMEM((k_part1<H, false>), (int)smP);
     HG_LAUNCH("hg_part1", (k_part1<H, false>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
               po->M, po->c_start, out1, nullptr, nullptr);
   }
   if (L.two_level) {
     auto part2 = [&](auto kern, const char* name, uint16_t* pm, uint32_t* mt) -> int {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+      HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));  // (kern is a runtime pointer: no per-site cache)
       HG_LAUNCH(name, kern, L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp, fine_cursor, out2, pm, mt);
       return HG_OK;
     };
@@ -2058,12 +2058,12 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
     lmap = ws.take<uint32_t>(n + 4);
     if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small for a traced build");
     const size_t smR = (size_t)kUnpStaged * 4;
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_repart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    HG_SET_SMEM((k_repart<1>), (int)smR);
     uint32_t* a1 = L.two_level ? reinterpret_cast<uint32_t*>(po.out1) : a2;  // level-1 keys are dead after part2
     HG_LAUNCH("hg_repart1", k_repart<1>, L.grid, kT, smR, st, nullptr, a1, po.pmap1, po.meta1, L.sub, L.nb1, L.tile, n,
               L.chunk, po.M, po.c_start, po.tp);
     if (L.two_level) {
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_repart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+      HG_SET_SMEM((k_repart<2>), (int)smR);
       HG_LAUNCH("hg_repart2", k_repart<2>, L.grid, kT, smR, st, a1, a2, po.pmap2, po.meta2, L.sub, L.nb1, L.tile, n,
                 L.chunk, po.M, po.c_start, po.tp);
     }
@@ -2071,11 +2071,11 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   const K* grouped = (const K*)po.grouped;  // build: == edges (two levels) or the level-1 buffer; traced: workspace
   const size_t smC = LocalPShape<K>::smem(L.s);
   if (traced) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+    HG_SET_SMEM((k_local_build_p<H, true>), (int)smC);
     HG_LAUNCH("hg_local_build_traced", (k_local_build_p<H, true>), num_sms(), LocalPShape<K>::kThreads, smC, st, grouped,
               po.fine_start, L.nfine, hp, L.s, v, offsets, edges, a2, positions, lmap);
   } else {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_build_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smC));
+    HG_SET_SMEM((k_local_build_p<H>), (int)smC);
     HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
               L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr);
   }
@@ -2086,11 +2086,11 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   const int copy = (L.two_level && !traced) ? 1 : 0;
   K* src = copy ? (K*)po.out1 : (K*)grouped;
   const size_t smBig = (size_t)(1u << L.s) * 4;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_count<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_SET_SMEM((k_big_count<H>), (int)smBig);
   const uint32_t* huge_list = po.big_list + L.nfine - 1;  // grows downwards (k_starts)
   HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, (K*)po.out1, copy, po.fine_start,
             po.big_list, huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges, a2, positions, lmap);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_big_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smBig));
+  HG_SET_SMEM((k_big_place<H>), (int)smBig);
   HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, huge_list,
             po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges, a2, positions, lmap);
   return HG_OK;
@@ -2108,7 +2108,7 @@ static int probe_stage(const uint32_t* t_off, const KeyOf<H>* t_edges, const Key
   HG_LAUNCH("hg_probe_plan", k_probe_plan, (L.nfine + 255) / 256, 256, 0, st, t_off, q_start, L.nfine, L.s, v,
             LocalShape<K>::kCap, pb.item_x, pb.big_bin, plan);
   const size_t smQ = probe_smem(L.s, sizeof(K) * 8);
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_local_probe<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smQ));
+  HG_SET_SMEM((k_local_probe<H>), (int)smQ);
   HG_LAUNCH("hg_local_probe", k_local_probe<H>, L.nfine + pb.max_extra, kT, smQ, st, t_off, t_edges, qpart, q_start,
             L.nfine, pb.item_x, plan, pb.big_bin, hp, L.s, v, pb.mult_bo, reinterpret_cast<unsigned long long*>(agg));
   if (pb.hs) {  // oversized table slices: key -> count hash table over the whole grid
@@ -2142,13 +2142,13 @@ static int query_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n
   const size_t smR = unpart_smem();
   uint32_t* level1_vals = reinterpret_cast<uint32_t*>(po.out1);  // level-1 keys are dead by now
   if (L.two_level) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    HG_SET_SMEM((k_unpart<2>), (int)smR);
     HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, mult_bo, level1_vals, po.pmap2, po.meta2, L.sub, L.nb1, L.tile,
               q, L.chunk, po.M, po.c_start, po.tp);
   } else {
     level1_vals = mult_bo;
   }
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+  HG_SET_SMEM((k_unpart<1>), (int)smR);
   HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, level1_vals, mult, po.pmap1, po.meta1, L.sub, L.nb1, L.tile, q,
             L.chunk, po.M, po.c_start, po.tp);
   return HG_OK;
@@ -2250,17 +2250,17 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
     return HG_OK;
   }
   const BinLayout& L = *Lt;
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_perm_bins, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kPermCap * 4)));
+  HG_SET_SMEM((k_perm_bins), (int)(kPermCap * 4));
   HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, kPermCap * 4, st, pb.mult_bo, lmap, tpo.fine_start, vals);
   const size_t smR = unpart_smem();
   uint32_t* l1 = vals;
   if (L.two_level) {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+    HG_SET_SMEM((k_unpart<2>), (int)smR);
     HG_LAUNCH("hg_unpart2", k_unpart<2>, L.grid, kT, smR, st, vals, level1, tpo.pmap2, tpo.meta2, L.sub, L.nb1, L.tile, q,
               L.chunk, tpo.M, tpo.c_start, tpo.tp);
     l1 = level1;
   }
-  HG_CHECK_CUDA(cudaFuncSetAttribute(k_unpart<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smR));
+  HG_SET_SMEM((k_unpart<1>), (int)smR);
   HG_LAUNCH("hg_unpart1", k_unpart<1>, L.grid, kT, smR, st, l1, mult, tpo.pmap1, tpo.meta1, L.sub, L.nb1, L.tile, q, L.chunk,
             tpo.M, tpo.c_start, tpo.tp);
   return HG_OK;

@@ -8,6 +8,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include <cstdio>
@@ -30,6 +32,21 @@ void note_launch_end(cudaStream_t s);
   do {                                                             \
     cudaError_t _e = (expr);                                       \
     if (_e != cudaSuccess) return ::hg::cuda_error(_e, #expr);     \
+  } while (0)
+
+// Opt a kernel into `bytes` of dynamic shared memory, once per call site and
+// device (the attribute is per device; the driver call costs microseconds,
+// which adds up over the many small builds of virtual shards).
+#define HG_SET_SMEM(kernel, bytes)                                                                 \
+  do {                                                                                             \
+    static std::atomic<int> _hg_smem_set[16];                                                      \
+    int _hg_dev = 0;                                                                               \
+    HG_CHECK_CUDA(cudaGetDevice(&_hg_dev));                                                        \
+    const int _hg_b = (int)(bytes);                                                                \
+    if (_hg_dev >= 16 || _hg_b > _hg_smem_set[_hg_dev].load(std::memory_order_relaxed)) {         \
+      HG_CHECK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, _hg_b)); \
+      if (_hg_dev < 16) _hg_smem_set[_hg_dev].store(_hg_b, std::memory_order_relaxed);             \
+    }                                                                                              \
   } while (0)
 
 // Launch a kernel with bookkeeping; returns from the enclosing function on a

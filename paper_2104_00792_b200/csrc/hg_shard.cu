@@ -485,9 +485,9 @@ static int reorg_count(const void* keys, uint64_t n, int key_bits, const HashPar
   const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
   const size_t smem_c = 8 * (shards + 1) + 4 * shards;
   if (key_bits == 32)
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_count<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+    HG_SET_SMEM((k_reorg_count<uint32_t>), (int)smem_c);
   else
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_count<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+    HG_SET_SMEM((k_reorg_count<uint64_t>), (int)smem_c);
   if (key_bits == 32) {
     HG_LAUNCH("hg_reorg_count", k_reorg_count<uint32_t>, (unsigned)tiles, kReorgWarps * 32, smem_c, s,
               (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts,
@@ -514,9 +514,9 @@ static int reorg_place(const void* keys, uint64_t n, int key_bits, const HashPar
   const auto* db = (const unsigned long long*)dest_base;
   // up to 224 KB at 4096 shards (reorg_check bounds the shard count by the opt-in limit)
   if (key_bits == 32)
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_place<uint32_t, kPeer>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+    HG_SET_SMEM((k_reorg_place<uint32_t, kPeer>), (int)smem_p);
   else
-    HG_CHECK_CUDA(cudaFuncSetAttribute(k_reorg_place<uint64_t, kPeer>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+    HG_SET_SMEM((k_reorg_place<uint64_t, kPeer>), (int)smem_p);
   if (key_bits == 32) {
     HG_LAUNCH("hg_reorg_place", (k_reorg_place<uint32_t, kPeer>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
               (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, (uint32_t*)grouped,
@@ -550,7 +550,7 @@ static int route_launch(const K* keys, uint64_t n, const HashParams& hp, const D
                         const unsigned long long* db, K* grouped, uint32_t* order, unsigned long long* cur,
                         uint64_t tiles, size_t smem, cudaStream_t s) {
   auto go = [&](auto kern) -> int {
-    HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  // runtime pointer
     HG_LAUNCH("hg_route", kern, (unsigned)tiles, kReorgWarps * 32, smem, s, keys, n, hp, dp, sp, shards, ro, dpt, db,
               grouped, order, cur);
     return HG_OK;
@@ -583,9 +583,9 @@ int hg_bin_histogram(const void* keys, uint64_t n, int key_bits, int kind, uint3
   int grid = use_smem ? num_sms() : grid_cap(n, 16);
   if (use_smem) {
     if (key_bits == 32)
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_bin_hist<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      HG_SET_SMEM((k_bin_hist<uint32_t>), (int)smem);
     else
-      HG_CHECK_CUDA(cudaFuncSetAttribute(k_bin_hist<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      HG_SET_SMEM((k_bin_hist<uint64_t>), (int)smem);
   }
   size_t dyn = use_smem ? smem : 0;
   if (key_bits == 32)
