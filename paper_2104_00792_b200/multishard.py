@@ -449,7 +449,46 @@ def _report(config, n, hr, bins_g, phase_ns, search_steps, keys_moved, bytes_mov
     )
 
 
+_side_streams = {}
+
+
+def _streams_for(dev, count):
+    """Cached side streams of a device (the shards' Phase-4 builds run concurrently)."""
+    t = D.torch()
+    key = (dev.index if hasattr(dev, "index") else int(dev))
+    ss = _side_streams.setdefault(key, [])
+    while len(ss) < count:
+        ss.append(t.cuda.Stream(device=dev))
+    return ss[:count]
+
+
 def _local_tables(received, config, key_bits):
+    """Phase 4 (multishard.py:403-409).  Virtual shards sharing one GPU build
+    concurrently on side streams (each build alone underfills the GPU; the
+    reference runs them on threads, multishard.py:414-419); the current stream
+    waits for all of them."""
+    t = D.torch()
+    devs = {r.device for r in received}
+    if len(received) > 1 and len(devs) == 1 and all(r.numel() for r in received):
+        dev = next(iter(devs))
+        with D.on(dev):
+            main = t.cuda.current_stream()
+            ready = t.cuda.Event()
+            ready.record(main)
+            tables = []
+            for r, ss in zip(received, _streams_for(dev, len(received))):
+                ss.wait_event(ready)
+                with t.cuda.stream(ss):
+                    v_d = hash_range_for(r.numel(), config.load_factor)
+                    off, edges, _ = build_device(r, v_d, config.family, key_bits)
+                    done = t.cuda.Event()
+                    done.record(ss)
+                main.wait_event(done)
+                r.record_stream(ss)  # (the input slice is read on ss)
+                off.record_stream(main)
+                edges.record_stream(main)
+                tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits, r.numel()))
+        return tables
     tables = []
     for r in received:
         v_d = hash_range_for(r.numel(), config.load_factor)

@@ -20,3 +20,12 @@ for label, parts, p in (("one", [one], 1), ("eight", eight, 8)):
         ts.append(rep.total_time_ns)
     ph = {k: v.time_ns for k, v in rep.phases.items()}
     print(label, "median total us", sorted(ts)[3] / 1e3, "phases us", {k: v / 1e3 for k, v in ph.items()}, flush=True)
+
+# host-side profile of one 8-shard build
+import cProfile, pstats  # noqa: E402
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(5):
+    hg.build_sharded(eight, hg.ShardConfig(shards=8, family=fam))
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
