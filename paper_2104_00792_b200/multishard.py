@@ -449,45 +449,30 @@ def _report(config, n, hr, bins_g, phase_ns, search_steps, keys_moved, bytes_mov
     )
 
 
-_side_streams = {}
-
-
-def _streams_for(dev, count):
-    """Cached side streams of a device (the shards' Phase-4 builds run concurrently)."""
-    t = D.torch()
-    key = (dev.index if hasattr(dev, "index") else int(dev))
-    ss = _side_streams.setdefault(key, [])
-    while len(ss) < count:
-        ss.append(t.cuda.Stream(device=dev))
-    return ss[:count]
-
-
 def _local_tables(received, config, key_bits):
-    """Phase 4 (multishard.py:403-409).  Virtual shards sharing one GPU build
-    concurrently on side streams (each build alone underfills the GPU; the
-    reference runs them on threads, multishard.py:414-419); the current stream
-    waits for all of them."""
+    """Phase 4 (multishard.py:403-409): one local build per shard with its
+    own range V_d = ceil(N_d / C).  Virtual shards sharing one GPU reuse one
+    workspace and call the library directly: a 2^20-key shard builds in tens
+    of microseconds, so per-call host overhead is what a loop over shards
+    would otherwise spend."""
     t = D.torch()
     devs = {r.device for r in received}
-    if len(received) > 1 and len(devs) == 1 and all(r.numel() for r in received):
+    if len(received) > 1 and len(devs) == 1:
+        lib = _lib.load()
+        kind, seed = family_code(config.family)
         dev = next(iter(devs))
         with D.on(dev):
-            main = t.cuda.current_stream()
-            ready = t.cuda.Event()
-            ready.record(main)
+            vds = [hash_range_for(r.numel(), config.load_factor) for r in received]
+            ws = D.workspace(max(lib.hg_build_workspace_size(r.numel(), v, key_bits) for r, v in zip(received, vds)))
+            stream = D.stream_ptr()
             tables = []
-            for r, ss in zip(received, _streams_for(dev, len(received))):
-                ss.wait_event(ready)
-                with t.cuda.stream(ss):
-                    v_d = hash_range_for(r.numel(), config.load_factor)
-                    off, edges, _ = build_device(r, v_d, config.family, key_bits)
-                    done = t.cuda.Event()
-                    done.record(ss)
-                main.wait_event(done)
-                r.record_stream(ss)  # (the input slice is read on ss)
-                off.record_stream(main)
-                edges.record_stream(main)
-                tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits, r.numel()))
+            for r, v_d in zip(received, vds):
+                off = t.empty(v_d + 1, dtype=t.int32, device=dev)
+                edges = t.empty(r.numel(), dtype=r.dtype, device=dev)
+                _lib.call("hg_build", r.data_ptr(), r.numel(), key_bits, kind, seed, v_d, off.data_ptr(),
+                          edges.data_ptr(), None, ws.data_ptr(), ws.numel(), stream)
+                tables.append(HashGraph(off, edges, v_d, config.family, float(config.load_factor), key_bits,
+                                        r.numel()))
         return tables
     tables = []
     for r in received:
