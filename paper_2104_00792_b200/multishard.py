@@ -507,6 +507,7 @@ def _build_sharded_one_device(per_shard_inputs, config, key_bits, dev):
         flat, sizes = _concat_inputs(per_shard_inputs, key_bits)
         n = flat.numel()
         hr, bins_g, bin_size = config.resolve(n)
+        t.cuda.current_stream().synchronize()  # inputs resident (the host->device copy is asynchronous) before the clock
         wall0 = time.perf_counter_ns()
         ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
         steps = t.zeros(1, dtype=t.int64, device=D.device())
