@@ -34,19 +34,31 @@ void note_launch_end(cudaStream_t s);
     if (_e != cudaSuccess) return ::hg::cuda_error(_e, #expr);     \
   } while (0)
 
-// Opt a kernel into `bytes` of dynamic shared memory, once per call site and
-// device (the attribute is per device; the driver call costs microseconds,
-// which adds up over the many small builds of virtual shards).
-#define HG_SET_SMEM(kernel, bytes)                                                                 \
-  do {                                                                                             \
-    static std::atomic<int> _hg_smem_set[16];                                                      \
-    int _hg_dev = 0;                                                                               \
-    HG_CHECK_CUDA(cudaGetDevice(&_hg_dev));                                                        \
-    const int _hg_b = (int)(bytes);                                                                \
-    if (_hg_dev >= 16 || _hg_b > _hg_smem_set[_hg_dev].load(std::memory_order_relaxed)) {         \
-      HG_CHECK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, _hg_b)); \
-      if (_hg_dev < 16) _hg_smem_set[_hg_dev].store(_hg_b, std::memory_order_relaxed);             \
-    }                                                                                              \
+// Opt a kernel into dynamic shared memory: once per call site and device the
+// kernel's limit is raised to the device's opt-in maximum (a permission, not
+// an allocation: each launch still asks for its own size), so call sites of
+// the same kernel never lower each other's limit.  The driver call costs
+// microseconds, which adds up over the many small builds of virtual shards.
+int smem_optin_max();
+template <typename F>
+cudaError_t smem_raise_limit(F kernel) {
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_optin_max() - (int)fa.sharedSizeBytes);
+}
+#define HG_SET_SMEM(kernel, bytes)                                                                   \
+  do {                                                                                               \
+    static std::atomic<bool> _hg_smem_done[16];                                                      \
+    int _hg_dev = 0;                                                                                 \
+    HG_CHECK_CUDA(cudaGetDevice(&_hg_dev));                                                          \
+    if ((int)(bytes) > ::hg::smem_optin_max())                                                       \
+      return ::hg::set_error(HG_ERR_CONFIG, "kernel needs %d bytes of shared memory", (int)(bytes)); \
+    if (_hg_dev >= 16 || !_hg_smem_done[_hg_dev].load(std::memory_order_acquire)) {                  \
+      HG_CHECK_CUDA(::hg::smem_raise_limit(kernel));                                                 \
+      if (_hg_dev < 16) _hg_smem_done[_hg_dev].store(true, std::memory_order_release);               \
+    }                                                                                                \
   } while (0)
 
 // Launch a kernel with bookkeeping; returns from the enclosing function on a

@@ -86,6 +86,26 @@ const char* hg_version(void) { return "hashgraph_b200 0.1.0 (sm_100a)"; }
 
 const char* hg_last_error(void) { return hg::t_error.c_str(); }
 
+}  // extern "C"
+
+namespace hg {
+// opt-in shared memory per block of the current device (static + dynamic)
+int smem_optin_max() {
+  static std::atomic<int> cache[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = dev < 16 ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (v <= 0) v = 232448;
+    if (dev < 16) cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+}  // namespace hg
+
+extern "C" {
+
 uint64_t hg_launch_count(void) { return hg::g_launches.load(); }
 
 void hg_timing_enable(int on) { hg::g_timing = on != 0; }
