@@ -336,8 +336,8 @@ __device__ __forceinline__ uint32_t smap_slot(K key) {
 }
 
 // Add `add` occurrences of key (all-ones key counted in *ones); false once the
-// map holds more than M / 2 distinct keys or a probe sequence runs long (the
-// caller flags overflow and stops streaming).
+// map holds more than M / 2 distinct keys (the caller flags overflow and stops
+// streaming).
 template <typename K>
 __device__ __forceinline__ bool smap_add(K* mk, uint32_t* mc, uint32_t* claimed, uint32_t* ones, K key, uint32_t add) {
   constexpr uint32_t M = SliceMapShape<K>::kSlots;
@@ -345,9 +345,12 @@ __device__ __forceinline__ bool smap_add(K* mk, uint32_t* mc, uint32_t* claimed,
     atomicAdd(ones, add);
     return true;
   }
-  if (*(volatile uint32_t*)claimed > M / 2) return false;  // too many distinct keys: give up early
+  // too many distinct keys: give up early (the caller's final check agrees:
+  // claimed only grows, so every work item of the bin decides the same way)
+  if (*(volatile uint32_t*)claimed > M / 2) return false;
   uint32_t i = smap_slot(key) & (M - 1);
-  for (uint32_t probe = 0; probe < 256; probe++, i = (i + 1) & (M - 1)) {
+  // claimed <= M/2 + one pending claim per thread < M here: an empty slot exists
+  for (uint32_t probe = 0; probe < M; probe++, i = (i + 1) & (M - 1)) {
     K cur = mk[i];
     if (cur == ~K(0)) {
       cur = cas_key(mk + i, ~K(0), key);
