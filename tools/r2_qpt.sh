@@ -1,6 +1,6 @@
 #!/bin/bash
-# probe batch-size variants (GPU box)
-for v in "" q32_4 q32_8 q64_4 q64_6; do
+# probe tail-unroll variants (GPU box)
+for v in "" tu2 tu4; do
   lib=""; [ -n "$v" ] && lib="HG_LIB=paper_2104_00792_b200/exp/$v.so"
   for a in "" "--load-factor 4" "--key-bits 64"; do
   env $lib timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3 $a 2>/dev/null | python tools/bench_line.py "[${v:-base} $a]" | cut -c1-140
