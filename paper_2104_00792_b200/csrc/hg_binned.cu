@@ -1738,7 +1738,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
     // relative to tlo, three loads in flight per thread; the bin's depth
     // classes (sorted / map) are flagged on the way
     const uint4* o4 = reinterpret_cast<const uint4*>(t_off + first);
-    uint32_t dmx = 0;  // deepest bucket seen by this thread
+    uint32_t flags = 0;
     constexpr int R = 3;
     for (uint32_t w0 = threadIdx.x; 4 * w0 <= nb; w0 += R * blockDim.x) {
       uint4 x[R];
@@ -1762,18 +1762,20 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
         const uint32_t w = w0 + r * blockDim.x, i0 = 4 * w;
         if (i0 > nb) break;
         // degrees of buckets i0..i0+3 (only those below nb exist)
-        dmx = max(max(dmx, i0 + 1 <= nb ? x[r].y - x[r].x : 0u), i0 + 2 <= nb ? x[r].z - x[r].y : 0u);
-        dmx = max(max(dmx, i0 + 3 <= nb ? x[r].w - x[r].z : 0u), i0 + 4 <= nb ? nx[r] - x[r].w : 0u);
+        const uint32_t dg[4] = {i0 + 1 <= nb ? x[r].y - x[r].x : 0u, i0 + 2 <= nb ? x[r].z - x[r].y : 0u,
+                                i0 + 3 <= nb ? x[r].w - x[r].z : 0u, i0 + 4 <= nb ? nx[r] - x[r].w : 0u};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          flags |= dg[e] > kBigDeg ? (uint32_t)kBinMap : 0u;
+          flags |= (dg[e] > kLinDeg && dg[e] <= kSortMax) ? (uint32_t)kBinSort : 0u;
+        }
         const uint32_t lo2 = ((x[r].x - tlo) & 0xFFFFu) | ((x[r].y - tlo) << 16);
         const uint32_t hi2 = ((x[r].z - tlo) & 0xFFFFu) | ((x[r].w - tlo) << 16);
         reinterpret_cast<uint2*>(off16)[w] = make_uint2(lo2, hi2);
       }
     }
     __syncthreads();  // s_flags initialised
-    // depth classes from the deepest bucket (a bin whose deep buckets are all
-    // above kSortMax also scans for sorted-class buckets and finds none)
-    dmx = __reduce_max_sync(0xffffffffu, dmx);
-    const uint32_t flags = (dmx > kLinDeg ? (uint32_t)kBinSort : 0u) | (dmx > kBigDeg ? (uint32_t)kBinMap : 0u);
+    flags = __reduce_or_sync(0xffffffffu, flags);
     if (flags && (threadIdx.x & 31) == 0) atomicOr(&s_flags, flags);
     if (threadIdx.x == 0 && ebytes) mbar_wait(&s_bar, 0);
   }
