@@ -382,6 +382,7 @@ k_route_claim(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
     }
   }
   __syncthreads();
+  __shared__ uint32_t s_cnt[MAXP > 0 ? MAXP : 1], s_toff[MAXP > 0 ? MAXP : 1];
   for (uint32_t d = threadIdx.x; d < shards; d += blockDim.x) {
     uint32_t run = 0;
     for (int w = 0; w < kReorgWarps; w++) {
@@ -390,16 +391,53 @@ k_route_claim(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
       run += c;
     }
     s_tb[d] = run ? atomicAdd(cursors + d, (unsigned long long)run) : 0ull;
+    if (MAXP > 0) s_cnt[d] = run;
   }
   __syncthreads();
+  if (MAXP > 0) {
+    // P <= 8: the tile's keys are staged destination-major in smem and every
+    // destination's run leaves as consecutive lanes' stores (full 32-byte
+    // sectors on NVLink / HBM) instead of one scattered store per key
+    K* st_k = reinterpret_cast<K*>(s_wcnt + kReorgWarps * shards);
+    uint32_t* st_o = reinterpret_cast<uint32_t*>(st_k + kReorgTile);
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+      for (uint32_t d = 0; d < shards; d++) {
+        s_toff[d] = acc;
+        acc += s_cnt[d];
+      }
+    }
+    __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kReorgPerLane; r++) {
-    if (dr[r] == 0xffffffffu) continue;
-    const uint32_t d = dr[r] >> 16;
-    const unsigned long long c = s_tb[d] + my[d] + (dr[r] & 0xFFFFu);
-    if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[dest_base[d] + c] = kv[r];
-    else grouped[row_offsets[d] + c] = kv[r];
-    if (order) order[row_offsets[d] + c] = (uint32_t)(wbase + r * 32 + lane);
+    for (int r = 0; r < kReorgPerLane; r++) {
+      if (dr[r] == 0xffffffffu) continue;
+      const uint32_t d = dr[r] >> 16;
+      const uint32_t slot = s_toff[d] + my[d] + (dr[r] & 0xFFFFu);
+      st_k[slot] = kv[r];
+      if (order) st_o[slot] = (uint32_t)(wbase + r * 32 + lane);
+    }
+    __syncthreads();
+    const uint32_t total = s_toff[shards - 1] + s_cnt[shards - 1];
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {  // consecutive threads: consecutive slots of a run
+      uint32_t d = 0;
+#pragma unroll
+      for (int dd = 1; dd < MAXP; dd++)
+        if ((uint32_t)dd < shards && i >= s_toff[dd]) d = dd;
+      const unsigned long long c = s_tb[d] + (i - s_toff[d]);
+      if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[dest_base[d] + c] = st_k[i];
+      else grouped[row_offsets[d] + c] = st_k[i];
+      if (order) order[row_offsets[d] + c] = st_o[i];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kReorgPerLane; r++) {
+      if (dr[r] == 0xffffffffu) continue;
+      const uint32_t d = dr[r] >> 16;
+      const unsigned long long c = s_tb[d] + my[d] + (dr[r] & 0xFFFFu);
+      if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[dest_base[d] + c] = kv[r];
+      else grouped[row_offsets[d] + c] = kv[r];
+      if (order) order[row_offsets[d] + c] = (uint32_t)(wbase + r * 32 + lane);
+    }
   }
   if (kPeer) __threadfence_system();
 }
@@ -690,7 +728,8 @@ int hg_route(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed
   HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
   DivParams dp = make_div_params(bin_size);
   const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
-  const size_t smem = 8 * (shards + 1) + 8 * (size_t)shards + 4 * (size_t)kReorgWarps * shards;
+  size_t smem = 8 * (shards + 1) + 8 * (size_t)shards + 4 * (size_t)kReorgWarps * shards;
+  if (shards <= 8) smem = (smem + 15) / 16 * 16 + (size_t)kReorgTile * (key_bits / 8 + 4);  // staged keys + input indices
   if (smem > 200 * 1024) return set_error(HG_ERR_CONFIG, "too many shards for hg_route (%u)", shards);
   const auto* ro = (const unsigned long long*)row_offsets;
   const auto* dpt = (const unsigned long long*)dest_ptrs;
