@@ -685,7 +685,7 @@ template <typename H, bool kQuery, uint32_t sub>  // sub = level-2 fan-out (128 
 __global__ void __launch_bounds__(kT, 2)
 k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1, const uint32_t* __restrict__ c_start,
         const uint32_t* __restrict__ tp_g, uint32_t* __restrict__ fine_cursor, KeyOf<H>* __restrict__ out,
-        uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta) {
+        uint16_t* __restrict__ pmap, uint32_t* __restrict__ meta, uint32_t c_lo = 0, uint32_t c_hi = 0xFFFFFFFFu) {
   using K = typename H::Key;
   using TS = TileShape<K>;
   constexpr int KPT = TS::kKPT;
@@ -701,7 +701,8 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     fence_proxy_async();
   }
   __syncthreads();
-  const uint32_t ntiles = s.tp[nb1];
+  const uint32_t ntiles = s.tp[min(c_hi, nb1)];  // level-1 bins [c_lo, c_hi): tiles [tp[c_lo], tp[c_hi])
+  const uint32_t tfirst = s.tp[min(c_lo, nb1)] + blockIdx.x;
   // thread 0 locates a tile (binary search over the level-2 tile prefix plus
   // two c_start loads) when it issues the tile's TMA, one tile ahead, and
   // leaves (bin, first element, size) in smem: no global latency at the top
@@ -724,9 +725,9 @@ k_part2(const KeyOf<H>* __restrict__ in, HashParams hp, int s_log, uint32_t nb1,
     tma_load_1d(s.raw, in + a0, bytes, &s.bar);
   };
   uint32_t parity = 0;
-  if (threadIdx.x == 0 && blockIdx.x < ntiles) locate_issue(blockIdx.x);
+  if (threadIdx.x == 0 && tfirst < ntiles) locate_issue(tfirst);
   __syncthreads();  // s_loc of the first tile (later ones are ordered by the tile loop's barriers)
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (uint32_t t = tfirst; t < ntiles; t += gridDim.x) {
     const uint32_t c = s_loc[0], t0 = s_loc[1], m = s_loc[2];
     if (!kQuery && threadIdx.x == 0) {  // build: re-read after ranking (measured: fewer spills); query: registers
       s_cur[0] = c;
@@ -1137,7 +1138,9 @@ template <typename H, bool kTrace = false>
 __global__ void __launch_bounds__(1024, 1)
 k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
                 uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges, const uint32_t* __restrict__ a2 = nullptr,
-                uint32_t* __restrict__ positions = nullptr, uint32_t* __restrict__ lmap = nullptr) {
+                uint32_t* __restrict__ positions = nullptr, uint32_t* __restrict__ lmap = nullptr, uint32_t f_lo = 0,
+                uint32_t f_hi = 0xFFFFFFFFu) {
+  f_hi = min(f_hi, nfine);  // this launch builds fine bins [f_lo, f_hi)
   using K = typename H::Key;
   using PS = LocalPShape<K>;
   constexpr int NT = PS::kThreads;
@@ -1155,7 +1158,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
   // (the offsets slice) of those above kHugeBin are zeroed here
   auto next_small = [&](uint32_t f) -> uint32_t {
     uint32_t sz;
-    while (f < nfine && (sz = fine_start[f + 1] - fine_start[f]) > kCap) {
+    while (f < f_hi && (sz = fine_start[f + 1] - fine_start[f]) > kCap) {
       if (sz > kHugeBin) {
         const uint64_t fb = (uint64_t)f << s;
         const uint32_t nbz = (uint32_t)min((uint64_t)S, v - fb);
@@ -1183,18 +1186,18 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     const uint32_t g = hi_cp + threadIdx.x;
     if (g >= lo && g < hi) raw[g - lo_al] = src[g];
   };
-  uint32_t f = next_small(blockIdx.x);
+  uint32_t f = next_small(f_lo + blockIdx.x);
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     fence_proxy_async();
   }
   __syncthreads();
-  if (f < nfine) fetch(f);
+  if (f < f_hi) fetch(f);
   // tail keys written by threads 0..VPL-1 (only for the array's last bin) are
   // visible after this barrier; later fetches are ordered by a bin's barriers
   __syncthreads();
   uint32_t parity = 0;
-  while (f < nfine) {
+  while (f < f_hi) {
     const uint32_t lo = fine_start[f], hi = fine_start[f + 1];
     const uint32_t cnt = hi - lo;
     const uint32_t lo_al = lo & ~(VPL - 1), sh = lo - lo_al;
@@ -1218,7 +1221,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     for (uint32_t i = threadIdx.x; i < ((nb + 1) / 2 + 3) / 4; i += NT)  // 16-byte stores (c16 is 128-byte padded)
       reinterpret_cast<uint4*>(c16)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();  // raw consumed, counters zero
-    if (fn < nfine) fetch(fn);
+    if (fn < f_hi) fetch(fn);
     // count: the atomic's old value is the key's rank inside its bucket.
     // Only the first and last chunk of a bin can be partial, so validity is
     // decided per chunk and full chunks run branch-free.  u32 keys keep only
@@ -1874,6 +1877,7 @@ struct PartOut {
   uint32_t* big_cp;     // build: oversized-bin chunk prefix (nfine + 1)
   uint32_t* big_done;   // build: their chunk-completion counters (2 x nfine)
   uint32_t* plan32;     // query: the probe plan words (zeroed by k_starts)
+  uint32_t* fine_cursor;
   uint32_t* M;
   uint32_t* fine_start;
   uint32_t* c_start;
@@ -1981,7 +1985,8 @@ size_t binned_ws_bytes(uint64_t n, const BinLayout& L, int key_bits, int mode, u
 // keys into `final_out`; otherwise they stay in workspace buffers.
 template <typename H>
 static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, const BinLayout& L, uint32_t cap,
-                         PartMode mode, KeyOf<H>* final_out, Workspace& ws, cudaStream_t st, PartOut* po) {
+                         PartMode mode, KeyOf<H>* final_out, Workspace& ws, cudaStream_t st, PartOut* po,
+                         bool skip_part2 = false) {
   using K = KeyOf<H>;
   const bool query = mode != kPartBuild;  // position maps + metadata
   uint32_t *fine_cnt, *fine_cursor;
@@ -2019,10 +2024,12 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
     HG_LAUNCH("hg_part1", (k_part1<H, false>), L.grid, kT, smP, st, keys, n, hp, L.shift1, L.bits1, L.nb1, L.chunk,
               po->M, po->c_start, out1, nullptr, nullptr);
   }
-  if (L.two_level) {
+  po->fine_cursor = fine_cursor;
+  if (L.two_level && !skip_part2) {
     auto part2 = [&](auto kern, const char* name, uint16_t* pm, uint32_t* mt) -> int {
       HG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));  // (kern is a runtime pointer: no per-site cache)
-      HG_LAUNCH(name, kern, L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp, fine_cursor, out2, pm, mt);
+      HG_LAUNCH(name, kern, L.grid, kT, smP, st, out1, hp, L.s, L.nb1, po->c_start, po->tp, fine_cursor, out2, pm, mt,
+                0u, 0xFFFFFFFFu);
       return HG_OK;
     };
     int rc2;
@@ -2033,9 +2040,6 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
       rc2 = L.sub == kSub ? part2(k_part2<H, false, kSub>, "hg_part2", nullptr, nullptr)
                           : part2(k_part2<H, false, kSubMax>, "hg_part2", nullptr, nullptr);
     if (rc2) return rc2;
-    po->grouped = out2;
-  } else {
-    po->grouped = out1;
   }
   return HG_OK;
 }
@@ -2049,9 +2053,28 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
                       KeyOf<H>* edges, Workspace& ws, cudaStream_t st, uint32_t* positions = nullptr) {
   using K = KeyOf<H>;
   const bool traced = positions != nullptr;
+  // experiment (HG_GROUPED=G): level-2 partition and local build alternate
+  // over groups of G level-1 bins, so the local build reads its bins while
+  // they are still in L2
+  static const int groups = getenv("HG_GROUPED") ? atoi(getenv("HG_GROUPED")) : 0;
+  const bool grouped_sched = groups > 0 && !traced && L.two_level;
   PartOut po{};
-  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, traced ? kPartTraced : kPartBuild, edges, ws, st, &po);
+  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, traced ? kPartTraced : kPartBuild, edges, ws, st, &po,
+                            grouped_sched);
   if (rc) return rc;
+  if (grouped_sched) {
+    const size_t smP = part_smem(sizeof(K) * 8), smC = LocalPShape<K>::smem(L.s);
+    HG_SET_SMEM((k_local_build_p<H>), (int)smC);
+    auto kp2 = L.sub == kSub ? k_part2<H, false, kSub> : k_part2<H, false, kSubMax>;
+    HG_CHECK_CUDA(cudaFuncSetAttribute(kp2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smP));
+    for (uint32_t c0 = 0; c0 < L.nb1; c0 += groups) {
+      const uint32_t c1 = std::min<uint32_t>(L.nb1, c0 + groups);
+      HG_LAUNCH("hg_part2", kp2, L.grid, kT, smP, st, (const K*)po.out1, hp, L.s, L.nb1, po.c_start, po.tp,
+                po.fine_cursor, edges, nullptr, nullptr, c0, c1);
+      HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, (const K*)edges,
+                po.fine_start, L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr, c0 * L.sub, c1 * L.sub);
+    }
+  }
   uint32_t *a2 = nullptr, *lmap = nullptr;
   if (traced) {
     a2 = ws.take<uint32_t>(n + 4);
@@ -2074,7 +2097,7 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
     HG_SET_SMEM((k_local_build_p<H, true>), (int)smC);
     HG_LAUNCH("hg_local_build_traced", (k_local_build_p<H, true>), num_sms(), LocalPShape<K>::kThreads, smC, st, grouped,
               po.fine_start, L.nfine, hp, L.s, v, offsets, edges, a2, positions, lmap);
-  } else {
+  } else if (!grouped_sched) {
     HG_SET_SMEM((k_local_build_p<H>), (int)smC);
     HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
               L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr);
