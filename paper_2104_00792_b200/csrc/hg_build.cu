@@ -420,6 +420,7 @@ int hg_intersect_tables(const uint32_t* offsets_a, const void* edges_a, uint64_t
                         void* workspace, size_t workspace_bytes, void* stream) {
   int rc = check_common(n_b, key_bits, kind, v);
   if (rc) return rc;
+  if (n_b && positions_b == nullptr) return set_error(HG_ERR_CONFIG, "positions_b is required");
   HashParams hp = make_hash_params(kind, seed, v, key_bits);
   cudaStream_t s = (cudaStream_t)stream;
   BinLayout Lp, Lt;
