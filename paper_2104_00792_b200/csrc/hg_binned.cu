@@ -1385,13 +1385,33 @@ struct ProbeQ {
   static constexpr int kQPT = sizeof(K) == 4 ? HG_PROBE_QPT : HG_PROBE_QPT64;
 };
 
+// Query slot k of a probe batch starting at q0 (a multiple of VPL = 16 /
+// sizeof(K)): each thread owns VPL consecutive queries per 16-byte group, so
+// a group loads with one 16-byte load and its counts leave with one store.
 template <typename K>
-__device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qhi, K (&qv)[ProbeQ<K>::kQPT]) {
-  constexpr int kProbeQPT = ProbeQ<K>::kQPT;
+__device__ __forceinline__ uint32_t qslot(uint32_t q0, int k) {
+  constexpr int VPL = 16 / sizeof(K);
+  return q0 + (uint32_t)(k / VPL) * (VPL * kT) + VPL * threadIdx.x + (uint32_t)(k % VPL);
+}
+
+// The batch at q0 of the bin's queries [qlo, qhi) (slots outside read as 0).
+template <typename K>
+__device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qlo, uint32_t qhi,
+                                             K (&qv)[ProbeQ<K>::kQPT]) {
+  constexpr int QPT = ProbeQ<K>::kQPT;
+  constexpr int VPL = 16 / sizeof(K);
 #pragma unroll
-  for (int k = 0; k < kProbeQPT; k++) {
-    const uint32_t j = q0 + k * kT + threadIdx.x;
-    qv[k] = j < qhi ? __ldcs(qpart + j) : K(0);
+  for (int g = 0; g < QPT / VPL; g++) {
+    const uint32_t j0 = qslot<K>(q0, g * VPL);
+    if (j0 >= qlo && j0 + VPL <= qhi) {
+      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(qpart + j0));
+      const K* xk = reinterpret_cast<const K*>(&x);
+#pragma unroll
+      for (int e = 0; e < VPL; e++) qv[g * VPL + e] = xk[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < VPL; e++) qv[g * VPL + e] = (j0 + e >= qlo && j0 + e < qhi) ? qpart[j0 + e] : K(0);
+    }
   }
 }
 
@@ -1522,20 +1542,23 @@ __device__ __noinline__ uint32_t sorted_count(const K* te, uint32_t a, uint32_t 
 }
 
 template <typename H, bool kFull>
-__device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const HashParams& hp, uint32_t first,
+__device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t qhi, const HashParams& hp, uint32_t first,
                                             const uint16_t* off16, const KeyOf<H>* te, const BigMap<KeyOf<H>>& map,
                                             bool overflow, uint32_t bin_flags, uint32_t* __restrict__ mult_bo,
                                             const KeyOf<H> (&qv)[ProbeQ<KeyOf<H>>::kQPT], uint32_t& m32, uint32_t& t32,
                                             uint32_t& d32) {
   using K = typename H::Key;
   constexpr int QPT = ProbeQ<K>::kQPT;
-  const uint32_t kmax = kFull ? (uint32_t)QPT : (qhi - q0 + kT - 1) / kT;  // query slots this batch fills
+  constexpr int VPL = 16 / sizeof(K);
+  auto valid = [&](int k) {
+    const uint32_t j = qslot<K>(q0, k);
+    return kFull || (j >= qlo && j < qhi);
+  };
   uint32_t ae[QPT];
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
     ae[k] = 0;
-    if (!kFull && (uint32_t)k >= kmax) continue;
-    if (kFull || q0 + k * kT + threadIdx.x < qhi) {
+    if (valid(k)) {
       const uint32_t l = H::bucket(qv[k], hp) - first;
       ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
     }
@@ -1550,9 +1573,10 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
   // site each, outside the unrolled loop: the loop stays small enough for the
   // instruction cache and no registers are saved around calls inside it)
   uint32_t rare = 0;
+  constexpr bool kVecOut = sizeof(K) == 4;  // (64-bit keys: registers are short, counts stored one by one)
+  uint32_t cv[kVecOut ? QPT : 1];
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
-    if (!kFull && (uint32_t)k >= kmax) break;
     const K q = qv[k];
     const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
     const bool mapped = use_map && d > kBigDeg;
@@ -1566,17 +1590,30 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       const K x = in ? te[a + t] : K(0);
       c += (uint32_t)(in & (x == q));
     }
-    const uint32_t j = q0 + k * kT + threadIdx.x;
-    if (kFull || j < qhi) {
+    if (kVecOut) cv[k % (kVecOut ? QPT : 1)] = c;
+    if (valid(k)) {
       d32 += d;
       if (mapped || srt) {
         rare |= 1u << k;
       } else {
-        mult_bo[j] = c;
+        if (!kVecOut) mult_bo[qslot<K>(q0, k)] = c;
         m32 += (c != 0);
         t32 += c;
       }
     }
+  }
+  if (!kVecOut) {
+  } else if (kFull && rare == 0) {  // VPL consecutive counts per store
+#pragma unroll
+    for (int g = 0; g < QPT / VPL; g++) {
+      uint32_t* p = mult_bo + qslot<K>(q0, g * VPL);
+      *reinterpret_cast<uint4*>(p) = make_uint4(cv[(g * VPL) % QPT], cv[(g * VPL + 1) % QPT], cv[(g * VPL + 2) % QPT],
+                                                cv[(g * VPL + 3) % QPT]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < QPT; k++)
+      if (valid(k) && !((rare >> k) & 1u)) mult_bo[qslot<K>(q0, k)] = cv[k % (kVecOut ? QPT : 1)];
   }
   while (rare) {
     const int k = __ffs(rare) - 1;
@@ -1591,7 +1628,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qhi, const Has
       }
     const uint32_t a = e & 0xFFFFu, d = (e >> 16) - a;
     const uint32_t c = d > kBigDeg ? map_count(map, q) : sorted_count<K>(te, a, d, q);
-    mult_bo[q0 + k * kT + threadIdx.x] = c;
+    mult_bo[qslot<K>(q0, k)] = c;
     m32 += (c != 0);
     t32 += c;
   }
@@ -1608,15 +1645,18 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
   constexpr int QPT = ProbeQ<K>::kQPT;
   constexpr uint32_t B = QPT * kT;
   K qn[QPT];  // the next batch, in flight while this one is probed
-  for (uint32_t q0 = qlo; q0 < qhi; q0 += B) {
-    if (q0 != qlo) {
+  const uint32_t qa = qlo & ~(16u / (uint32_t)sizeof(K) - 1);  // batches start 16-byte aligned
+  for (uint32_t q0 = qa; q0 < qhi; q0 += B) {
+    if (q0 != qa) {
 #pragma unroll
       for (int k = 0; k < QPT; k++) qv[k] = qn[k];  // (the first batch was loaded before staging)
     }
-    if (q0 + B < qhi) load_queries<K>(qpart, q0 + B, qhi, qn);
+    if (q0 + B < qhi) load_queries<K>(qpart, q0 + B, qlo, qhi, qn);
     uint32_t m32 = 0, t32 = 0, d32 = 0;
-    if (!HG_PROBE_NOFULL && qhi - q0 >= B) probe_batch<H, true>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
-    else probe_batch<H, false>(q0, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
+    if (!HG_PROBE_NOFULL && q0 >= qlo && qhi - q0 >= B)
+      probe_batch<H, true>(q0, qlo, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
+    else
+      probe_batch<H, false>(q0, qlo, qhi, hp, first, off16, te, map, overflow, bin_flags, mult_bo, qv, m32, t32, d32);
     matched += m32;
     total += t32;
     comps += d32;
@@ -1708,7 +1748,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
   if (qlo >= qhi) return;
   K qv[ProbeQ<K>::kQPT];
-  load_queries<K>(qpart, qlo, qhi, qv);  // first batch in flight during staging
+  load_queries<K>(qpart, qlo & ~(16u / (uint32_t)sizeof(K) - 1), qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
