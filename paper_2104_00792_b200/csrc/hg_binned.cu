@@ -1385,12 +1385,18 @@ struct ProbeQ {
   static constexpr int kQPT = sizeof(K) == 4 ? HG_PROBE_QPT : HG_PROBE_QPT64;
 };
 
-// Query slot k of a probe batch starting at q0 (a multiple of VPL = 16 /
-// sizeof(K)): each thread owns VPL consecutive queries per 16-byte group, so
-// a group loads with one 16-byte load and its counts leave with one store.
+// Query slot k of a probe batch starting at q0 (a multiple of QVec<K>):
+// 32-bit keys -- each thread owns groups of 4 consecutive queries, so a group
+// loads with one 16-byte load and its counts leave with one 16-byte store;
+// 64-bit keys -- one query per slot, strided by the CTA (2-key groups measured
+// slower: their extra live registers spill).
+template <typename K>
+struct QVec {
+  static constexpr int kV = sizeof(K) == 4 ? 4 : 1;
+};
 template <typename K>
 __device__ __forceinline__ uint32_t qslot(uint32_t q0, int k) {
-  constexpr int VPL = 16 / sizeof(K);
+  constexpr int VPL = QVec<K>::kV;
   return q0 + (uint32_t)(k / VPL) * (VPL * kT) + VPL * threadIdx.x + (uint32_t)(k % VPL);
 }
 
@@ -1399,11 +1405,11 @@ template <typename K>
 __device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32_t q0, uint32_t qlo, uint32_t qhi,
                                              K (&qv)[ProbeQ<K>::kQPT]) {
   constexpr int QPT = ProbeQ<K>::kQPT;
-  constexpr int VPL = 16 / sizeof(K);
+  constexpr int VPL = QVec<K>::kV;
 #pragma unroll
   for (int g = 0; g < QPT / VPL; g++) {
     const uint32_t j0 = qslot<K>(q0, g * VPL);
-    if (j0 >= qlo && j0 + VPL <= qhi) {
+    if (VPL == 4 && j0 >= qlo && j0 + VPL <= qhi) {
       const uint4 x = __ldcs(reinterpret_cast<const uint4*>(qpart + j0));
       const K* xk = reinterpret_cast<const K*>(&x);
 #pragma unroll
@@ -1549,7 +1555,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
                                             uint32_t& d32) {
   using K = typename H::Key;
   constexpr int QPT = ProbeQ<K>::kQPT;
-  constexpr int VPL = 16 / sizeof(K);
+  constexpr int VPL = QVec<K>::kV;
   auto valid = [&](int k) {
     const uint32_t j = qslot<K>(q0, k);
     return kFull || (j >= qlo && j < qhi);
@@ -1645,7 +1651,7 @@ __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ 
   constexpr int QPT = ProbeQ<K>::kQPT;
   constexpr uint32_t B = QPT * kT;
   K qn[QPT];  // the next batch, in flight while this one is probed
-  const uint32_t qa = qlo & ~(16u / (uint32_t)sizeof(K) - 1);  // batches start 16-byte aligned
+  const uint32_t qa = qlo & ~((uint32_t)QVec<K>::kV - 1);  // batches start at a group boundary
   for (uint32_t q0 = qa; q0 < qhi; q0 += B) {
     if (q0 != qa) {
 #pragma unroll
@@ -1748,7 +1754,7 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
   uint32_t qhi = min(q_start[f + 1], qlo + kProbeChunk);
   if (qlo >= qhi) return;
   K qv[ProbeQ<K>::kQPT];
-  load_queries<K>(qpart, qlo & ~(16u / (uint32_t)sizeof(K) - 1), qlo, qhi, qv);  // first batch in flight during staging
+  load_queries<K>(qpart, qlo & ~((uint32_t)QVec<K>::kV - 1), qlo, qhi, qv);  // first batch in flight during staging
   const uint64_t first = (uint64_t)f << s;
   const uint32_t nb = (uint32_t)min((uint64_t)S, v - first);
   const uint32_t tlo = t_off[first], thi = t_off[first + nb];
