@@ -1414,9 +1414,11 @@ __device__ __forceinline__ void load_queries(const K* __restrict__ qpart, uint32
       const K* xk = reinterpret_cast<const K*>(&x);
 #pragma unroll
       for (int e = 0; e < VPL; e++) qv[g * VPL + e] = xk[e];
+    } else if (VPL == 1) {  // (batches start at qlo)
+      qv[g] = j0 < qhi ? __ldcs(qpart + j0) : K(0);
     } else {
 #pragma unroll
-      for (int e = 0; e < VPL; e++) qv[g * VPL + e] = (j0 + e >= qlo && j0 + e < qhi) ? qpart[j0 + e] : K(0);
+      for (int e = 0; e < VPL; e++) qv[g * VPL + e] = (j0 + e >= qlo && j0 + e < qhi) ? __ldcs(qpart + j0 + e) : K(0);
     }
   }
 }
@@ -1558,7 +1560,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
   constexpr int VPL = QVec<K>::kV;
   auto valid = [&](int k) {
     const uint32_t j = qslot<K>(q0, k);
-    return kFull || (j >= qlo && j < qhi);
+    return kFull || ((VPL == 1 || j >= qlo) && j < qhi);  // (VPL == 1: batches start at qlo)
   };
   uint32_t ae[QPT];
 #pragma unroll
