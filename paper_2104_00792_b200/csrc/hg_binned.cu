@@ -1562,10 +1562,13 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
     const uint32_t j = qslot<K>(q0, k);
     return kFull || ((VPL == 1 || j >= qlo) && j < qhi);  // (VPL == 1: batches start at qlo)
   };
+  // query slots this batch can fill (whole groups of VPL)
+  const uint32_t kmax = kFull ? (uint32_t)QPT : (qhi - q0 + VPL * kT - 1) / (VPL * kT) * VPL;
   uint32_t ae[QPT];
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
     ae[k] = 0;
+    if (!kFull && (uint32_t)k >= kmax) continue;
     if (valid(k)) {
       const uint32_t l = H::bucket(qv[k], hp) - first;
       ae[k] = (uint32_t)off16[l] | ((uint32_t)off16[l + 1] << 16);
@@ -1585,6 +1588,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
   uint32_t cv[kVecOut ? QPT : 1];
 #pragma unroll
   for (int k = 0; k < QPT; k++) {
+    if (!kFull && (uint32_t)k >= kmax) break;
     const K q = qv[k];
     const uint32_t a = ae[k] & 0xFFFFu, d = (ae[k] >> 16) - a;
     const bool mapped = use_map && d > kBigDeg;
