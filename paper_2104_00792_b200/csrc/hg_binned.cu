@@ -1258,10 +1258,9 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       }
     }
     __syncthreads();
-    // the previous bin's edges have left staged by the time the scan's last
-    // barrier passes (its bulk store was issued a whole bin ago)
-    if (threadIdx.x == 0) tma_store_wait_read();
     scan_c16_offsets(c16, nb, lo, offsets + first);
+    if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
+    __syncthreads();
     K* stg = staged + sh;
     auto place_key = [&](K key, int k, uint32_t g) {
       uint32_t rel;
