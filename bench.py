@@ -200,6 +200,25 @@ def measured_peak():
 # --------------------------------------------------------------------------- CPU baseline
 
 
+def host_info() -> dict:
+    """CPU model and RAM of the host the CPU arm runs on (BASELINE.md asks for both)."""
+    model, ram_gb = "unknown", None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    ram_gb = round(int(line.split()[1]) / (1 << 20), 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "ram_gb": ram_gb, "hw_threads": os.cpu_count()}
+
+
 def cpu_sample(log2: int, k: int, lf: float, workers: int):
     """Reference algorithm (oracle restatement) on a bounded sample: build +
     query of 2^log2 keys / queries of the bench workload's streams."""
@@ -248,7 +267,8 @@ def run_reference(args, rank, world):
         "config": {"workload": workload_name(args), "keys_per_gpu": 1 << args.log2_keys,
                    "queries_per_gpu": 1 << args.log2_keys,
                    "sample": f"each step times 2^{log2} keys + 2^{log2} queries of the same streams on the host"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -511,7 +531,7 @@ def main():
     if not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         val, tb, tq = cpu_sample(args.cpu_log2, args.k, args.load_factor, workers)
-        cpu = {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
+        cpu = {"value": val, "unit": UNIT, "cores": workers, "kind": "port", "host": host_info(),
                "sample": (f"2^{args.cpu_log2} keys + 2^{args.cpu_log2} queries of the same streams (k={args.k}, "
                           f"C={args.load_factor}); build {tb:.2f} s + query {tq:.2f} s with the numpy restatement "
                           f"of the reference (oracle/), worker_count={workers}")}
