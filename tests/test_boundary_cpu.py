@@ -39,6 +39,22 @@ def test_workspace_queries_are_host_only():
     assert lib.hg_reorganize_workspace_size(1 << 20, 8) > 0
 
 
+def test_two_step_abi_host_checks():
+    """hg_build_traced_workspace_size covers the trace on top of the build;
+    hg_intersect_tables sizes its workspace and rejects a missing positions
+    array before touching the device."""
+    lib = _lib.load()
+    n = 1 << 22
+    assert lib.hg_build_traced_workspace_size(n, n, 32) > lib.hg_build_workspace_size(n, n, 32) + 16 * n
+    assert lib.hg_build_traced_workspace_size(100, 100, 32) == lib.hg_build_workspace_size(100, 100, 32)  # direct path
+    assert lib.hg_intersect_tables_workspace_size(n, n, n, 32) > 8 * n
+    rc = lib.hg_intersect_tables(None, None, n, None, None, None, n, 32, 0, 0, n, None, 0, None, None, None, 0, None)
+    assert rc == -1 and b"positions_b" in lib.hg_last_error()
+    # layouts beyond 32768 fine bins (2^30 keys at C = 1) stay on the binned path's workspace
+    big = 1 << 30
+    assert lib.hg_build_workspace_size(big, big, 32) > 4 * big
+
+
 def test_config_errors_match_reference_types():
     assert issubclass(hg.ConfigError, ValueError)
     assert issubclass(hg.SnapshotFormatError, RuntimeError)
