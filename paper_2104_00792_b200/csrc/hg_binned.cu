@@ -1433,10 +1433,7 @@ constexpr uint32_t kLinDeg = 16;
 constexpr uint32_t kSortMax = 1024;
 constexpr uint32_t kBigDeg = kSortMax;  // buckets deeper than this use the map
 constexpr uint32_t kMapSlots = 256;     // open addressing, power of two
-// depth classes present in a bin; kBinShallow: some non-empty bucket at or
-// below kBigDeg (a bin without one -- every query either misses or lands in a
-// map bucket, e.g. C3's buckets of 4096 copies -- takes the map-only loop)
-enum : uint32_t { kBinSort = 1, kBinMap = 2, kBinShallow = 4 };
+enum : uint32_t { kBinSort = 1, kBinMap = 2 };  // depth classes present in a bin
 
 template <typename K>
 struct BigMap {
@@ -1649,50 +1646,6 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
   }
 }
 
-// Bins whose non-empty buckets are all map buckets: a query's count is 0 (empty
-// bucket) or its map entry; no slots, tails or searches.
-template <typename K>
-__device__ __forceinline__ uint32_t map_count_inl(const BigMap<K>& m, K key) {
-  uint32_t i = map_slot(key);
-  for (uint32_t probe = 0; probe < kMapSlots; probe++, i = (i + 1) & (kMapSlots - 1)) {
-    if (m.state[i] == 0) return 0;
-    if (m.key[i] == key) return m.cnt[i];
-  }
-  return 0;
-}
-
-template <typename H>
-__device__ __noinline__ void probe_queries_map(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
-                                               const HashParams& hp, uint32_t first, const uint16_t* off16,
-                                               const BigMap<KeyOf<H>>& map, uint32_t* __restrict__ mult_bo,
-                                               KeyOf<H> (&qv)[ProbeQ<KeyOf<H>>::kQPT], uint64_t& matched,
-                                               uint64_t& total, uint64_t& comps) {
-  using K = KeyOf<H>;
-  constexpr int QPT = ProbeQ<K>::kQPT;
-  constexpr uint32_t B = QPT * kT;
-  const uint32_t qa = qlo & ~((uint32_t)QVec<K>::kV - 1);
-  for (uint32_t q0 = qa; q0 < qhi; q0 += B) {
-    if (q0 != qa) load_queries<K>(qpart, q0, qlo, qhi, qv);
-    uint32_t m32 = 0, t32 = 0, d32 = 0;
-#pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const uint32_t j = qslot<K>(q0, k);
-      if (j >= qlo && j < qhi) {
-        const uint32_t l = H::bucket(qv[k], hp) - first;
-        const uint32_t d = (uint32_t)off16[l + 1] - off16[l];
-        const uint32_t c = d ? map_count_inl(map, qv[k]) : 0u;
-        mult_bo[j] = c;
-        m32 += c != 0;
-        t32 += c;
-        d32 += d;
-      }
-    }
-    matched += m32;
-    total += t32;
-    comps += d32;
-  }
-}
-
 template <typename H>
 __device__ __forceinline__ void probe_queries_smem(const KeyOf<H>* __restrict__ qpart, uint32_t qlo, uint32_t qhi,
                                                    const HashParams& hp, uint32_t first, const uint16_t* off16,
@@ -1870,7 +1823,6 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
         for (int e = 0; e < 4; e++) {
           flags |= dg[e] > kBigDeg ? (uint32_t)kBinMap : 0u;
           flags |= (dg[e] > kLinDeg && dg[e] <= kSortMax) ? (uint32_t)kBinSort : 0u;
-          flags |= (dg[e] != 0 && dg[e] <= kBigDeg) ? (uint32_t)kBinShallow : 0u;
         }
         const uint32_t lo2 = ((x[r].x - tlo) & 0xFFFFu) | ((x[r].y - tlo) << 16);
         const uint32_t hi2 = ((x[r].z - tlo) & 0xFFFFu) | ((x[r].w - tlo) << 16);
@@ -1943,11 +1895,8 @@ k_local_probe(const uint32_t* __restrict__ t_off, const KeyOf<H>* __restrict__ t
 #if defined(HG_EXP_PROBE) && HG_EXP_PROBE == 3  // timing experiment (tools/build_variant.py): first batch only
   qhi = min(qhi, qlo + ProbeQ<K>::kQPT * kT);
 #endif
-  if ((bin_flags & (kBinMap | kBinShallow)) == kBinMap && !overflow)
-    probe_queries_map<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, map, mult_bo, qv, matched, total, comps);
-  else
-    probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, bin_flags, mult_bo, qv,
-                          matched, total, comps);
+  probe_queries_smem<H>(qpart, qlo, qhi, hp, (uint32_t)first, off16, te, map, overflow, bin_flags, mult_bo, qv, matched,
+                        total, comps);
   if (agg) flush_agg(matched, total, comps, agg);
 }
 
