@@ -4,7 +4,11 @@
 keys), u32 two-level (2^17 keys over V = 2^24: 1024 fine bins, 8 level-1
 bins), a high-duplicate table (oversized fine bins, deep-bucket probe map)
 and u64 two-level, each checked against the oracle so a sanitizer run also
-proves the answers."""
+proves the answers.  Round 2 adds: sorted deep buckets (V = N / 64),
+all-identical keys (the chunked oversized-bin build, the hash-table query
+path, hot-bin probe items), identical queries against a uniform table, the
+65536-fine-bin layout, and the two-step query (traced build, k_repart,
+k_perm_bins; the scatter path for foreign positions)."""
 
 import os
 import sys
@@ -34,6 +38,19 @@ def main():
     k64 = O.generate_keys(64, n, 7, key_bits=64)
     case(k64, np.concatenate([k64[: n // 2], O.generate_keys(64, n // 2, 8, key_bits=64)]), hash_range=1 << 22,
          key_bits=64)
+    case(O.generate_keys(17, n, 9), O.generate_keys(17, n, 10), hash_range=n // 64)  # sorted deep buckets
+    same = np.full(n, 7, np.uint32)
+    case(same, np.concatenate([same[: n // 2], O.generate_keys(17, n // 2, 11)]))  # chunked build, hash table
+    case(O.generate_keys(17, n, 12), np.full(n, 99, np.uint32))  # hot bin: extra probe items
+    k = O.generate_keys(32, n // 2, 13)
+    table = hg.build(k, hash_range=1 << 30)  # 65536 fine bins
+    assert np.array_equal(hg.intersect(table, k[::3]).multiplicities, O.count_occurrences(k, k[::3]))
+    keys, queries = O.generate_keys(17, n, 14), O.generate_keys(17, n, 15)
+    table = hg.build(keys)
+    qt, pos = hg.build_query_table(table, queries)  # traced build
+    want = O.count_occurrences(keys, queries)
+    assert np.array_equal(hg.intersect_tables(table, qt, pos).multiplicities, want)  # through the trace
+    assert np.array_equal(hg.intersect_tables(table, qt, pos.copy()).multiplicities, want)  # scatter
     print("sanitize_case ok")
 
 
