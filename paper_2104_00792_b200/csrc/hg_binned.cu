@@ -1374,6 +1374,10 @@ __device__ __forceinline__ void flush_agg(uint64_t matched, uint64_t total, uint
 #ifndef HG_PROBE_QPT64
 #define HG_PROBE_QPT64 8
 #endif
+#ifndef HG_TAIL_UNROLL
+#define HG_TAIL_UNROLL 4  // (experiment knob: unroll of the probe's linear tail)
+#endif
+constexpr int kTailUnroll = HG_TAIL_UNROLL;
 #ifndef HG_PROBE_NOFULL
 #define HG_PROBE_NOFULL 0  // experiment: one batch variant (bounds-checked) instead of two
 #endif
@@ -1597,6 +1601,7 @@ __device__ __forceinline__ void probe_batch(uint32_t q0, uint32_t qlo, uint32_t 
     uint32_t c = (uint32_t)((d > 0) & (e0 == q)) + (uint32_t)((d > 1) & (e1 == q)) +
                  (uint32_t)((d > 2) & (e2 == q)) + (uint32_t)((d > 3) & (e3 == q));
     const uint32_t dmax = __reduce_max_sync(0xffffffffu, mapped || srt ? 0u : d);
+#pragma unroll kTailUnroll
     for (uint32_t t = 4; t < dmax; t++) {
       const bool in = t < d;
       const K x = in ? te[a + t] : K(0);
