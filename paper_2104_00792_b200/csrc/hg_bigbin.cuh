@@ -566,16 +566,17 @@ __global__ void __launch_bounds__(kHtT) k_ht_insert(const uint32_t* __restrict__
   const uint32_t total = (uint32_t)plan[kPlanBigT];
   const uint64_t cap = plan[kPlanCap];
   __shared__ uint32_t s_j;
-  for (uint32_t c0 = blockIdx.x * CH; c0 < total; c0 += gridDim.x * CH) {
-    if (threadIdx.x == 0) s_j = upper_index(big_t, nbig, c0);
+  // (64-bit chunk cursor: totals can approach 2^32 and the stride must not wrap)
+  for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < total; c0 += (uint64_t)gridDim.x * CH) {
+    if (threadIdx.x == 0) s_j = upper_index(big_t, nbig, (uint32_t)c0);
     __syncthreads();
     const uint32_t j0 = s_j;
     __syncthreads();
-    const uint32_t e0 = c0 + threadIdx.x * kHtKPT;
+    const uint64_t e0 = c0 + threadIdx.x * kHtKPT;
     K cur = K(0);
     uint32_t run = 0;
     for (int u = 0; u < kHtKPT; u++) {
-      const uint32_t e = e0 + u;
+      const uint32_t e = (uint32_t)min(e0 + u, (uint64_t)total);  // (== total: past the end)
       bool flush = false;
       K key = K(0);
       if (e < total) {
@@ -625,16 +626,17 @@ __global__ void __launch_bounds__(kHtT) k_ht_lookup(const KeyOf<H>* __restrict__
   const uint32_t ones = (uint32_t)plan[kPlanOnes];
   __shared__ uint32_t s_j[2];
   uint64_t matched = 0, tot = 0, comps = 0;
-  for (uint32_t c0 = blockIdx.x * CH; c0 < total; c0 += gridDim.x * CH) {
-    if (threadIdx.x == 0) s_j[0] = upper_index(big_q, nbig, c0);
-    if (threadIdx.x == 1) s_j[1] = upper_index(big_q, nbig, min(total, c0 + CH) - 1);
+  for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < total; c0 += (uint64_t)gridDim.x * CH) {
+    if (threadIdx.x == 0) s_j[0] = upper_index(big_q, nbig, (uint32_t)c0);
+    if (threadIdx.x == 1) s_j[1] = upper_index(big_q, nbig, (uint32_t)(min((uint64_t)total, c0 + CH) - 1));
     __syncthreads();
     const uint32_t ja = s_j[0], jz = s_j[1];
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-      const uint32_t e = c0 + u * kHtT + threadIdx.x;
-      if (e < total) {
+      const uint64_t e64 = c0 + u * kHtT + threadIdx.x;
+      const uint32_t e = (uint32_t)e64;
+      if (e64 < total) {
         uint32_t a = ja, z = jz + 1;  // big_q[a] <= e < big_q[z]
         while (z - a > 1) {
           const uint32_t m = (a + z) >> 1;
