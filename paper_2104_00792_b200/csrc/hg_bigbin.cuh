@@ -95,19 +95,17 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
   __syncthreads();
   constexpr int U = BigShape<K>::kKPT;  // keys per thread per round (a bin of <= kChunk keys: one round)
   const uint32_t step = U * blockDim.x;
-  // rounds advance by `rem` tests (r0 + step may pass 2^32 for the last bin of a huge table)
-  for (uint32_t r0 = lo; r0 < hi; r0 = hi - r0 > step ? r0 + step : hi) {
-    const uint32_t rem = hi - r0;
+  for (uint32_t r0 = lo; r0 < hi; r0 += step) {
     K kv[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t o = u * blockDim.x + threadIdx.x;
-      kv[u] = o < rem ? src[r0 + o] : K(0);
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t o = u * blockDim.x + threadIdx.x, e = r0 + o;
-      const bool ok = o < rem;
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      const bool ok = e < hi;
       if (ok && copy) dst[e] = kv[u];
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
@@ -119,17 +117,16 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) offsets[first + i] = cnt[i];
   __syncthreads();
   const K* from = copy ? dst : src;
-  for (uint32_t r0 = lo; r0 < hi; r0 = hi - r0 > step ? r0 + step : hi) {
-    const uint32_t rem = hi - r0;
+  for (uint32_t r0 = lo; r0 < hi; r0 += step) {
     K kv[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t o = u * blockDim.x + threadIdx.x;
-      kv[u] = o < rem ? from[r0 + o] : K(0);
+      const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
+      kv[u] = e < hi ? from[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const bool ok = u * blockDim.x + threadIdx.x < rem;
+      const bool ok = r0 + u * blockDim.x + threadIdx.x < hi;
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
       uint32_t b0 = 0;
@@ -180,13 +177,13 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
     K kv[BS::kKPT];
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t o = u * BS::kThreads + threadIdx.x, e = lo + o;
-      kv[u] = o < hi - lo ? src[e] : K(0);
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t o = u * BS::kThreads + threadIdx.x, e = lo + o;
-      const bool ok = o < hi - lo;
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = e < hi;
       if (ok && copy) dst[e] = kv[u];
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
@@ -236,13 +233,13 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
     uint32_t lr[BS::kKPT];  // bucket << 15 | rank (bucket < 2^14, rank < kChunk <= 2^14)
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t o = u * BS::kThreads + threadIdx.x, e = lo + o;
-      kv[u] = o < hi - lo ? src[e] : K(0);
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      kv[u] = e < hi ? src[e] : K(0);
     }
 #pragma unroll
     for (int u = 0; u < BS::kKPT; u++) {
-      const uint32_t o = u * BS::kThreads + threadIdx.x, e = lo + o;
-      const bool ok = o < hi - lo;
+      const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
+      const bool ok = e < hi;
       const uint32_t l = ok ? H::bucket(kv[u], hp) - (uint32_t)first : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, l);
       uint32_t b0 = 0;
@@ -262,7 +259,7 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
         const uint32_t slot = cnt[lr[u] >> 15] + (lr[u] & 0x7FFFu);
         edges[slot] = kv[u];
         if (a2) {  // traced build
-          const uint32_t o = u * BS::kThreads + threadIdx.x, e = lo + o;
+          const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
           positions[slot] = a2[e];
           lmap[e] = slot;
         }

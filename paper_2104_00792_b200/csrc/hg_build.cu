@@ -268,6 +268,9 @@ constexpr uint64_t kBinnedMin = 1ull << 16;  // below this the 3-kernel direct p
 
 static bool use_binned(uint64_t n_table, uint64_t n, uint64_t v, int key_bits, BinLayout* L) {
   if (n < kBinnedMin) return false;
+  // the binned kernels step 32-bit key cursors by up to 2^20 past a bin's
+  // start; the last 2^20 indices below 2^32 stay on the direct path
+  if (n > (1ull << 32) - (1ull << 20) || n_table > (1ull << 32) - (1ull << 20)) return false;
   if (getenv("HG_FORCE_DIRECT")) return false;
   return binned_layout(n_table, n, v, key_bits, L);
 }
