@@ -48,7 +48,16 @@ struct TileShape {
 template <typename K>
 struct LocalShape {
   static constexpr int kKPT = sizeof(K) == 4 ? 38 : 19;
-  static constexpr uint32_t kCap = kKPT * kT;  // keys per fine bin handled in smem
+  static constexpr uint32_t kCap = kKPT * kT;  // keys per fine bin the probe stages in smem
+};
+
+#ifndef HG_BUILD_KPT32
+#define HG_BUILD_KPT32 38
+#endif
+// keys per fine bin the local build holds in smem (bins above it: hg_bigbin.cuh)
+template <typename K>
+struct BuildShape {
+  static constexpr uint32_t kCap = (sizeof(K) == 4 ? HG_BUILD_KPT32 : 19) * kT;
 };
 
 
@@ -1123,7 +1132,7 @@ template <typename K>
 struct LocalPShape {
   static constexpr int kThreads = 1024;
   static constexpr int kVPL = 16 / sizeof(K);
-  static constexpr uint32_t kCap = LocalShape<K>::kCap;                      // keys per bin in smem
+  static constexpr uint32_t kCap = BuildShape<K>::kCap;                      // keys per bin in smem
   static constexpr uint32_t kChunks = (kCap + 2 * kVPL - 2) / kVPL;          // 16-byte chunks a bin spans
   static constexpr int kCPT = (kChunks + kThreads - 1) / kThreads;           // chunks per thread
   static constexpr uint32_t kElems = kChunks * kVPL;
@@ -2116,7 +2125,7 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   static const int groups = getenv("HG_GROUPED") ? atoi(getenv("HG_GROUPED")) : 0;
   const bool grouped_sched = groups > 0 && !traced && L.two_level;
   PartOut po{};
-  int rc = run_partition<H>(keys, n, hp, L, LocalShape<K>::kCap, traced ? kPartTraced : kPartBuild, edges, ws, st, &po,
+  int rc = run_partition<H>(keys, n, hp, L, BuildShape<K>::kCap, traced ? kPartTraced : kPartBuild, edges, ws, st, &po,
                             grouped_sched);
   if (rc) return rc;
   if (grouped_sched) {
