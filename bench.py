@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--key-bits", type=int, default=32, choices=[32, 64],
                     help="64: full SplitMix64 words as keys (BASELINE configs[3])")
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-depth", type=int, default=3, help="e2e steps in flight (one stream and output buffer each)")
     ap.add_argument("--cpu-log2", type=int, default=24, help="CPU baseline sample size 2^x")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -445,19 +446,20 @@ def main():
         hq = torch.empty(q, dtype=sdt, pin_memory=True)
         hk.copy_(keys.cpu())
         hq.copy_(queries.cpu())
-        # Two steps in flight on two streams (a serving loop): step i+1's H2D
-        # overlaps step i's kernels and D2H; PCIe is full duplex, so the step
-        # rate is bounded by the 2 GiB of inputs per step.  The host consumes
+        # `depth` steps in flight, one stream each (a serving loop): step
+        # i+1's H2D overlaps step i's kernels and D2H; PCIe is full duplex, so
+        # the step rate is bounded by the 2 GiB of inputs per step.  The host consumes
         # every step's result (waits for its D2H, reads it) before reusing
         # that step's output buffer.
-        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-        outs = [torch.empty(q, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        done = [None, None]
+        depth = args.e2e_depth
+        streams = [torch.cuda.Stream() for _ in range(depth)]
+        outs = [torch.empty(q, dtype=torch.int32, pin_memory=True) for _ in range(depth)]
+        done = [None] * depth
         checksum = 0
 
         def e2e_step(i):
             nonlocal checksum
-            slot = i % 2
+            slot = i % depth
             if done[slot] is not None:
                 done[slot].synchronize()
                 checksum ^= int(outs[slot][0])  # the host reads the previous result of this slot
@@ -474,10 +476,10 @@ def main():
                 done[slot] = ev
             return res
 
-        for i in range(2):
+        for i in range(depth):
             e2e_step(i)
         torch.cuda.synchronize()
-        done = [None, None]
+        done = [None] * depth
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -494,7 +496,8 @@ def main():
         e2e = {"value": (n + q) * world * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": (kb // 8) * (n + q), "d2h_bytes_per_step": 4 * q,
                "ms_per_step": e2e_s / args.e2e_steps * 1e3,
-               "pipeline": "2 steps in flight on 2 streams; host waits for and reads each result before reusing its buffer"}
+               "pipeline": f"{depth} steps in flight on {depth} streams; host waits for and reads each result before reusing its buffer"}
+        e2e["link"] = pcie_link(hk, outs[0], e2e)
 
     # end to end as a caller of the reference API sees it: numpy keys and
     # queries in, build + intersect, then the int64 multiplicities and the
@@ -551,6 +554,54 @@ def main():
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def pcie_link(h_in, h_out, e2e):
+    """The host link's own copy rates, measured here (pinned buffers, CUDA
+    events, best of 3): H2D alone, D2H alone, and one step's copies with
+    nothing else running -- its input bytes H2D on one stream while its
+    result bytes go D2H on another.  That duplex time is the floor of a
+    serving loop whose compute hides under the copies; `frac` = floor / the
+    measured e2e step."""
+    import torch
+
+    d_in = torch.empty(h_in.numel(), dtype=h_in.dtype, device="cuda")
+    d_out = torch.empty(h_out.numel(), dtype=h_out.dtype, device="cuda")
+    in_b, out_b = h_in.numel() * h_in.element_size(), h_out.numel() * h_out.element_size()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    reps_in = max(1, round(e2e["h2d_bytes_per_step"] / in_b))  # copies of h_in per step's inputs
+    reps_out = max(1, round(e2e["d2h_bytes_per_step"] / out_b))
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            s_in.wait_stream(torch.cuda.current_stream())
+            s_out.wait_stream(torch.cuda.current_stream())
+            fn()
+            torch.cuda.current_stream().wait_stream(s_in)
+            torch.cuda.current_stream().wait_stream(s_out)
+            b.record()
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return best
+
+    def up():
+        with torch.cuda.stream(s_in):
+            for _ in range(reps_in):
+                d_in.copy_(h_in, non_blocking=True)
+
+    def down():
+        with torch.cuda.stream(s_out):
+            for _ in range(reps_out):
+                h_out.copy_(d_out, non_blocking=True)
+
+    t_up, t_down = timed(up), timed(down)
+    t_both = timed(lambda: (up(), down()))
+    return {"h2d_GBps": reps_in * in_b / t_up / 1e6, "d2h_GBps": reps_out * out_b / t_down / 1e6,
+            "step_copies_alone_ms": t_both, "frac": t_both / e2e["ms_per_step"]}
 
 
 def load_traffic(kernel: str):
