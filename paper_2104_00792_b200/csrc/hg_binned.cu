@@ -2250,6 +2250,15 @@ __global__ void k_qstart(const uint32_t* __restrict__ q_off, uint32_t nfine, int
   if (f <= nfine) q_start[f] = q_off[min((uint64_t)f << s, v)];
 }
 
+// Probe-layout bin starts from a trace grouped at a finer or equal layout
+// (fine bins nest: bin f of shift s_p is bins [f << d, (f + 1) << d) of shift
+// s_p - d, in the same ascending order).
+__global__ void k_qstart_nested(const uint32_t* __restrict__ fs, uint32_t nfine_t, uint32_t nfine_p, int d,
+                                uint32_t* __restrict__ q_start) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f <= nfine_p) q_start[f] = fs[min((uint64_t)f << d, (uint64_t)nfine_t)];
+}
+
 __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n,
                              uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -2330,8 +2339,20 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
     if (!tw.ok()) return set_error(HG_ERR_CONFIG, "trace buffer too small (%zu < %zu)", tw.cap, tw.used);
   }
   HG_CHECK_CUDA(cudaMemsetAsync(plan, 0, kPlanWords * 8, st));
-  HG_LAUNCH("hg_qstart", k_qstart, (Lp.nfine + 256) / 256, 256, 0, st, q_off, Lp.nfine, Lp.s, v, q_start);
-  int rc = probe_stage<H>(t_off, t_edges, q_edges, q_start, q, hp, v, Lp, plan, pb, agg, st);
+  // A trace grouped at the probe's layout or a finer one holds the query
+  // keys exactly as hg_query's partition leaves them (grouped by fine bin, in
+  // the order the position maps undo): the probe reads them there and its
+  // counts go straight back through the maps, as in the fused query.
+  const bool grouped = trace && Lt->s <= Lp.s;
+  int rc;
+  if (grouped) {
+    HG_LAUNCH("hg_qstart", k_qstart_nested, (Lp.nfine + 256) / 256, 256, 0, st, tpo.fine_start, Lt->nfine, Lp.nfine,
+              Lp.s - Lt->s, q_start);
+    rc = probe_stage<H>(t_off, t_edges, (const K*)tpo.grouped, q_start, q, hp, v, Lp, plan, pb, agg, st);
+  } else {
+    HG_LAUNCH("hg_qstart", k_qstart, (Lp.nfine + 256) / 256, 256, 0, st, q_off, Lp.nfine, Lp.s, v, q_start);
+    rc = probe_stage<H>(t_off, t_edges, q_edges, q_start, q, hp, v, Lp, plan, pb, agg, st);
+  }
   if (rc) return rc;
   const int g = num_sms() * 8;
   if (!trace) {
@@ -2339,8 +2360,12 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
     return HG_OK;
   }
   const BinLayout& L = *Lt;
-  HG_SET_SMEM((k_perm_bins), (int)(kPermCap * 4));
-  HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, kPermCap * 4, st, pb.mult_bo, lmap, tpo.fine_start, vals);
+  if (grouped) {
+    vals = pb.mult_bo;  // already in grouped order
+  } else {
+    HG_SET_SMEM((k_perm_bins), (int)(kPermCap * 4));
+    HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, kPermCap * 4, st, pb.mult_bo, lmap, tpo.fine_start, vals);
+  }
   const size_t smR = unpart_smem();
   uint32_t* l1 = vals;
   if (L.two_level) {

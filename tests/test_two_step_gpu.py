@@ -82,3 +82,14 @@ def test_build_traced_binned_positions():
     assert np.array_equal(np.sort(positions), np.arange(n))
     off, placed, _ = O.build_csr(keys, table.hash_range)
     assert np.array_equal(table.offset, off)
+
+
+@pytest.mark.parametrize("log2_t,log2_q", [(18, 21), (21, 17), (20, 20)])
+def test_two_step_layouts(log2_t, log2_q):
+    """Query tables larger than the table (the trace's fine bins nest inside
+    the probe's: the probe reads the trace's grouped keys), smaller (coarser
+    trace: the query table's own slices are probed and permuted back), and
+    equal (same layout)."""
+    keys = O.generate_keys(log2_t, 1 << log2_t, 0)
+    queries = O.generate_keys(log2_t, 1 << log2_q, 0x51)
+    two_step(keys, queries, 1 << log2_t)
