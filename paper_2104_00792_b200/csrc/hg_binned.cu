@@ -1280,7 +1280,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
         rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
       }
       stg[rel] = key;
-      if (kTrace) lmap[g] = lo + rel;
+      return rel;
     };
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
@@ -1288,12 +1288,22 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       const uint32_t e0 = c * VPL;
       if (c < nch) {
         if (e0 >= sh && e0 + VPL <= sh + cnt) {
+          uint32_t r[VPL];
 #pragma unroll
-          for (int j = 0; j < (int)VPL; j++) place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+          for (int j = 0; j < (int)VPL; j++) r[j] = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+          if (kTrace) {  // a full chunk's slots leave with one vector store (g = lo_al + e0 + j is VPL-aligned)
+            if (VPL == 4)
+              *reinterpret_cast<uint4*>(lmap + lo_al + e0) = make_uint4(lo + r[0], lo + r[1 % VPL], lo + r[2 % VPL], lo + r[3 % VPL]);
+            else
+              *reinterpret_cast<uint2*>(lmap + lo_al + e0) = make_uint2(lo + r[0], lo + r[1 % VPL]);
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
-            if (e0 + j - sh < cnt) place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+            if (e0 + j - sh < cnt) {
+              const uint32_t r = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+              if (kTrace) lmap[lo + e0 + j - sh] = lo + r;
+            }
         }
       }
     }
@@ -1319,7 +1329,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       if (threadIdx.x == 0) tma_store_wait_read();
       __syncthreads();
       uint32_t* st32 = reinterpret_cast<uint32_t*>(staged) + (lo & 3u);
-      auto place_pos = [&](K key, int k, uint32_t g) {
+      auto place_pos = [&](K key, int k, uint32_t a) {
         uint32_t rel;
         if (kRehash) {
           const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
@@ -1327,16 +1337,30 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
         } else {
           rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
         }
-        st32[rel] = a2[g];
+        st32[rel] = a;
       };
 #pragma unroll
       for (int i = 0; i < CPT; i++) {
         const uint32_t c = i * NT + threadIdx.x;
         const uint32_t e0 = c * VPL;
         if (c < nch) {
+          // the chunk's carried indices in one vector load (a2 is padded
+          // past n, and lo_al + e0 is VPL-aligned)
+          uint32_t av[VPL];
+          if (VPL == 4) {
+            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(a2 + lo_al + e0));
+            av[0] = x.x;
+            av[1 % VPL] = x.y;
+            av[2 % VPL] = x.z;
+            av[3 % VPL] = x.w;
+          } else {
+            const uint2 x = __ldcs(reinterpret_cast<const uint2*>(a2 + lo_al + e0));
+            av[0] = x.x;
+            av[1 % VPL] = x.y;
+          }
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
-            if (e0 + j - sh < cnt) place_pos(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
+            if (e0 + j - sh < cnt) place_pos(kv[i * VPL + j], i * VPL + j, av[j]);
         }
       }
       fence_proxy_async();
