@@ -51,9 +51,6 @@ struct LocalShape {
   static constexpr uint32_t kCap = kKPT * kT;  // keys per fine bin the probe stages in smem
 };
 
-#ifndef HG_TRACE_DIRECT
-#define HG_TRACE_DIRECT 0  // experiment knob: traced local build writes edges straight to global memory
-#endif
 #ifndef HG_BUILD_KPT32
 #define HG_BUILD_KPT32 38
 #endif
@@ -1292,14 +1289,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
     __syncthreads();
     K* stg = staged + sh;
-    // kDirect (traced builds, HG_TRACE_DIRECT): edges go straight to global
-    // memory from the placement loop and the positions take the staging
-    // buffer in the same pass (no second placement, no wait for the edges'
-    // bulk store)
-    constexpr bool kDirect = kTrace && HG_TRACE_DIRECT;
-    uint32_t* st32d = reinterpret_cast<uint32_t*>(staged) + (lo & 3u);
-    uint32_t av[VPL];
-    auto place_key = [&](K key, int k, uint32_t g, int j) {
+    auto place_key = [&](K key, int k, uint32_t g) {
       uint32_t rel;
       if (kRehash) {
         const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
@@ -1307,12 +1297,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       } else {
         rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
       }
-      if (kDirect) {
-        edges[lo + rel] = key;
-        st32d[rel] = av[j];
-      } else {
-        stg[rel] = key;
-      }
+      stg[rel] = key;
       return rel;
     };
 #pragma unroll
@@ -1320,23 +1305,10 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       const uint32_t c = i * NT + threadIdx.x;
       const uint32_t e0 = c * VPL;
       if (c < nch) {
-        if (kDirect) {
-          if (VPL == 4) {
-            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(a2 + lo_al + e0));
-            av[0] = x.x;
-            av[1 % VPL] = x.y;
-            av[2 % VPL] = x.z;
-            av[3 % VPL] = x.w;
-          } else {
-            const uint2 x = __ldcs(reinterpret_cast<const uint2*>(a2 + lo_al + e0));
-            av[0] = x.x;
-            av[1 % VPL] = x.y;
-          }
-        }
         if (e0 >= sh && e0 + VPL <= sh + cnt) {
           uint32_t r[VPL];
 #pragma unroll
-          for (int j = 0; j < (int)VPL; j++) r[j] = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh, j);
+          for (int j = 0; j < (int)VPL; j++) r[j] = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
           if (kTrace) {  // a full chunk's slots leave with one vector store (g = lo_al + e0 + j is VPL-aligned)
             if (VPL == 4)
               *reinterpret_cast<uint4*>(lmap + lo_al + e0) = make_uint4(lo + r[0], lo + r[1 % VPL], lo + r[2 % VPL], lo + r[3 % VPL]);
@@ -1347,7 +1319,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
             if (e0 + j - sh < cnt) {
-              const uint32_t r = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh, j);
+              const uint32_t r = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
               if (kTrace) lmap[lo + e0 + j - sh] = lo + r;
             }
         }
@@ -1358,17 +1330,17 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     // edges: aligned body by one bulk store, head and tail (< VPL each) by threads
     const uint32_t g0 = min(hi, (lo + VPL - 1) & ~(VPL - 1));
     const uint32_t g1 = max(g0, hi & ~(VPL - 1));
-    if (!kDirect && threadIdx.x == 0 && g1 > g0) {
+    if (threadIdx.x == 0 && g1 > g0) {
       tma_store_1d(edges + g0, staged + (g0 - lo_al), (g1 - g0) * (uint32_t)sizeof(K));
       tma_store_commit();
     }
-    if (!kDirect && threadIdx.x < VPL) {
+    if (threadIdx.x < VPL) {
       const uint32_t gh = lo + threadIdx.x;
       if (gh < g0) edges[gh] = staged[gh - lo_al];
       const uint32_t gt = g1 + threadIdx.x;
       if (gt < hi) edges[gt] = staged[gt - lo_al];
     }
-    if (kTrace && !kDirect) {
+    if (kTrace) {
       // positions through the same staging buffer once the edges have left
       // it: slot rel of the bin gets a2[g] of the key placed there, then one
       // bulk store (u32 view, 16-byte congruent to positions + lo)
@@ -1421,19 +1393,6 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
         if (gh < p0) positions[gh] = st32[gh - lo];
         const uint32_t gt = p1 + threadIdx.x;
         if (gt < hi) positions[gt] = st32[gt - lo];
-      }
-    }
-    if (kDirect) {  // positions were staged by the placement loop
-      const uint32_t p0 = min(hi, (lo + 3) & ~3u), p1 = max(p0, hi & ~3u);
-      if (threadIdx.x == 0 && p1 > p0) {
-        tma_store_1d(positions + p0, st32d + (p0 - lo), (p1 - p0) * 4u);
-        tma_store_commit();
-      }
-      if (threadIdx.x < 4) {
-        const uint32_t gh = lo + threadIdx.x;
-        if (gh < p0) positions[gh] = st32d[gh - lo];
-        const uint32_t gt = p1 + threadIdx.x;
-        if (gt < hi) positions[gt] = st32d[gt - lo];
       }
     }
     f = fn;
