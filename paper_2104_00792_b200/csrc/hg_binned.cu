@@ -1298,6 +1298,14 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
         rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
       }
       stg[rel] = key;
+      if (kTrace) {  // the slot replaces the rank: the positions pass needs no re-hash or counter load
+        if (kRehash) {
+          const int sft = (k & 1) * 16;
+          rk[k >> 1] = (rk[k >> 1] & ~(0xFFFFu << sft)) | (rel << sft);
+        } else {
+          rk[k] = rel;
+        }
+      }
       return rel;
     };
 #pragma unroll
@@ -1348,13 +1356,8 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       __syncthreads();
       uint32_t* st32 = reinterpret_cast<uint32_t*>(staged) + (lo & 3u);
       auto place_pos = [&](K key, int k, uint32_t a) {
-        uint32_t rel;
-        if (kRehash) {
-          const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
-          rel = get16(c16, l) + ((rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
-        } else {
-          rel = get16(c16, rk[k] >> 16) + (rk[k] & 0xFFFFu);
-        }
+        (void)key;
+        const uint32_t rel = kRehash ? (rk[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu : rk[k];  // slot from the edges pass
         st32[rel] = a;
       };
 #pragma unroll
