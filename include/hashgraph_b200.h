@@ -90,12 +90,14 @@ HG_API int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const ui
                  const void* edges_b, const uint32_t* positions_b, uint64_t n_b, int key_bits,
                  int kind, uint32_t seed, uint64_t v, uint32_t* mult, uint64_t* agg, void* stream);
 
-/* intersect_tables on the binned path (query.py:120-179): the query table's
- * fine-bin slices are probed against table A (the same depth classes,
- * sorted-bucket search and hash-table path as hg_query), counts return to
- * query order through `trace` (the workspace of the hg_build that produced
- * table B with positions, hg_build_traced_workspace_size bytes; nullable) or,
- * without a trace, by scattering through positions_b.  n_a = table A's key
+/* intersect_tables on the binned path (query.py:120-179), with the same depth
+ * classes, sorted-bucket search and hash-table path as hg_query.  With `trace`
+ * (the workspace of the hg_build that produced table B with positions,
+ * hg_build_traced_workspace_size bytes; nullable) grouped at table A's probe
+ * layout or a finer one, the trace's grouped query keys are probed and the
+ * counts return to query order through its position maps; a coarser trace
+ * probes table B's fine-bin slices and permutes the counts through the trace;
+ * without a trace the counts scatter through positions_b.  n_a = table A's key
  * count.  Small inputs run hg_intersect's kernels.  agg accumulated (caller
  * zeroes). */
 HG_API size_t hg_intersect_tables_workspace_size(uint64_t n_b, uint64_t v, uint64_t n_a, int key_bits);
