@@ -73,7 +73,7 @@ HG_API int hg_hash(const void* keys, uint64_t n, int key_bits, int kind, uint32_
 HG_API size_t hg_build_workspace_size(uint64_t n, uint64_t v, int key_bits);
 /* Workspace for hg_build with positions on the binned path (build_traced):
  * the workspace then also holds the build's TRACE (position maps of both
- * partition levels and each grouped key's edge slot), which
+ * partition levels, the grouped keys and their input indices), which
  * hg_intersect_tables reuses to return counts to input order by streaming
  * instead of scattering.  A smaller workspace runs the direct Alg. 1 kernels. */
 HG_API size_t hg_build_traced_workspace_size(uint64_t n, uint64_t v, int key_bits);
@@ -93,11 +93,11 @@ HG_API int hg_intersect(const uint32_t* offsets_a, const void* edges_a, const ui
 /* intersect_tables on the binned path (query.py:120-179), with the same depth
  * classes, sorted-bucket search and hash-table path as hg_query.  With `trace`
  * (the workspace of the hg_build that produced table B with positions,
- * hg_build_traced_workspace_size bytes; nullable) grouped at table A's probe
- * layout or a finer one, the trace's grouped query keys are probed and the
- * counts return to query order through its position maps; a coarser trace
- * probes table B's fine-bin slices and permutes the counts through the trace;
- * without a trace the counts scatter through positions_b.  n_a = table A's key
+ * hg_build_traced_workspace_size bytes; nullable), the trace's grouped query
+ * keys are probed (at table A's probe layout when the trace's fine bins nest in
+ * it, else at the trace's own) and the counts return to query order through its
+ * position maps; without a trace table B's fine-bin slices are probed and the
+ * counts scatter through positions_b.  n_a = table A's key
  * count.  Small inputs run hg_intersect's kernels.  agg accumulated (caller
  * zeroes). */
 HG_API size_t hg_intersect_tables_workspace_size(uint64_t n_b, uint64_t v, uint64_t n_a, int key_bits);

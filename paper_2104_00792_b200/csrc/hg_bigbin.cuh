@@ -87,7 +87,7 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
                                            uint32_t lo, uint32_t hi, uint64_t first, const HashParams& hp, int s,
                                            uint64_t v, uint32_t* cnt, uint32_t* __restrict__ offsets,
                                            KeyOf<H>* __restrict__ edges, const uint32_t* __restrict__ a2,
-                                           uint32_t* __restrict__ positions, uint32_t* __restrict__ lmap) {
+                                           uint32_t* __restrict__ positions) {
   using K = KeyOf<H>;
   const uint32_t nb = (uint32_t)min((uint64_t)1 << s, v - first);
   const uint32_t lt = lanemask_lt();
@@ -138,7 +138,6 @@ __device__ __forceinline__ void big_medium(const KeyOf<H>* __restrict__ src, Key
         if (a2) {  // traced build
           const uint32_t e = r0 + u * blockDim.x + threadIdx.x;
           positions[slot] = a2[e];
-          lmap[e] = slot;
         }
       }
     }
@@ -153,8 +152,7 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
                                                     const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_cp,
                                                     uint32_t* __restrict__ done, HashParams hp, int s, uint64_t v,
                                                     uint32_t* __restrict__ offsets, KeyOf<H>* __restrict__ edges,
-                                                    const uint32_t* __restrict__ a2, uint32_t* __restrict__ positions,
-                                                    uint32_t* __restrict__ lmap) {
+                                                    const uint32_t* __restrict__ a2, uint32_t* __restrict__ positions) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
@@ -165,7 +163,7 @@ __global__ void __launch_bounds__(1024) k_big_count(const KeyOf<H>* __restrict__
   for (uint32_t k = blockIdx.x; k < nmed; k += gridDim.x) {
     const uint32_t f = big_list[k];
     big_medium<H>(src, dst, copy, fine_start[f], fine_start[f + 1], (uint64_t)f << s, hp, s, v, cnt, offsets, edges, a2,
-                  positions, lmap);
+                  positions);
   }
   for (uint32_t k = blockIdx.x; k < nch; k += gridDim.x) {
     big_chunk(k, nbig, BS::kChunk, big_cp, huge_list, fine_start, s_loc);
@@ -213,7 +211,7 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
                                                     const uint32_t* __restrict__ big_cp, uint32_t* __restrict__ done,
                                                     HashParams hp, int s, uint64_t v, uint32_t* __restrict__ offsets,
                                                     KeyOf<H>* __restrict__ edges, const uint32_t* __restrict__ a2,
-                                                    uint32_t* __restrict__ positions, uint32_t* __restrict__ lmap) {
+                                                    uint32_t* __restrict__ positions) {
   using K = KeyOf<H>;
   using BS = BigShape<K>;
   extern __shared__ uint32_t cnt[];  // 2^s
@@ -261,7 +259,6 @@ __global__ void __launch_bounds__(1024) k_big_place(const KeyOf<H>* __restrict__
         if (a2) {  // traced build
           const uint32_t e = lo + u * BS::kThreads + threadIdx.x;
           positions[slot] = a2[e];
-          lmap[e] = slot;
         }
       }
     if (last_chunk(done, j, nck)) {

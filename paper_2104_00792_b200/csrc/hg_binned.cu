@@ -1159,13 +1159,13 @@ struct LocalPShape {
 };
 
 // kTrace (build_traced / build_query_table): also positions[p] = a2[g] (the
-// input index of grouped key g, from k_repart) and lmap[g] = p for the slot p
-// each grouped key lands in.
+// input index of grouped key g, from k_repart) for the slot p each grouped key
+// lands in.
 template <typename H, bool kTrace = false>
 __global__ void __launch_bounds__(1024, 1)
 k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, uint32_t nfine, HashParams hp, int s,
                 uint64_t v, uint32_t* __restrict__ offsets, KeyOf<H>* edges, const uint32_t* __restrict__ a2 = nullptr,
-                uint32_t* __restrict__ positions = nullptr, uint32_t* __restrict__ lmap = nullptr, uint32_t f_lo = 0,
+                uint32_t* __restrict__ positions = nullptr, uint32_t f_lo = 0,
                 uint32_t f_hi = 0xFFFFFFFFu) {
   f_hi = min(f_hi, nfine);  // this launch builds fine bins [f_lo, f_hi)
   using K = typename H::Key;
@@ -1289,7 +1289,7 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
     if (threadIdx.x == 0) tma_store_wait_read();  // the previous bin's edges have left staged
     __syncthreads();
     K* stg = staged + sh;
-    auto place_key = [&](K key, int k, uint32_t g) {
+    auto place_key = [&](K key, int k) {
       uint32_t rel;
       if (kRehash) {
         const uint32_t l = H::bucket(key, hp) - (uint32_t)first;
@@ -1306,7 +1306,6 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
           rk[k] = rel;
         }
       }
-      return rel;
     };
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
@@ -1314,22 +1313,12 @@ k_local_build_p(const KeyOf<H>* src, const uint32_t* __restrict__ fine_start, ui
       const uint32_t e0 = c * VPL;
       if (c < nch) {
         if (e0 >= sh && e0 + VPL <= sh + cnt) {
-          uint32_t r[VPL];
 #pragma unroll
-          for (int j = 0; j < (int)VPL; j++) r[j] = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
-          if (kTrace) {  // a full chunk's slots leave with one vector store (g = lo_al + e0 + j is VPL-aligned)
-            if (VPL == 4)
-              *reinterpret_cast<uint4*>(lmap + lo_al + e0) = make_uint4(lo + r[0], lo + r[1 % VPL], lo + r[2 % VPL], lo + r[3 % VPL]);
-            else
-              *reinterpret_cast<uint2*>(lmap + lo_al + e0) = make_uint2(lo + r[0], lo + r[1 % VPL]);
-          }
+          for (int j = 0; j < (int)VPL; j++) place_key(kv[i * VPL + j], i * VPL + j);
         } else {
 #pragma unroll
           for (int j = 0; j < (int)VPL; j++)
-            if (e0 + j - sh < cnt) {
-              const uint32_t r = place_key(kv[i * VPL + j], i * VPL + j, lo + e0 + j - sh);
-              if (kTrace) lmap[lo + e0 + j - sh] = lo + r;
-            }
+            if (e0 + j - sh < cnt) place_key(kv[i * VPL + j], i * VPL + j);
         }
       }
     }
@@ -2069,7 +2058,7 @@ static void probe_alloc(uint64_t q, const BinLayout& L, uint64_t n_table, Worksp
 
 // Workspace of a binned pass, by a dry run of the same carve-up the pass
 // performs (mode: kPartBuild / kPartQuery / kPartTraced; the query adds its
-// probe buffers, the traced build the carried input indices and lmap).
+// probe buffers, the traced build the carried input indices).
 template <typename K>
 static size_t ws_dry_run(uint64_t n, const BinLayout& L, PartMode mode, uint64_t n_table) {
   Workspace w{nullptr, ~(size_t)0, 0};
@@ -2082,7 +2071,6 @@ static size_t ws_dry_run(uint64_t n, const BinLayout& L, PartMode mode, uint64_t
     probe_alloc<K>(n, L, n_table, w, &pb);
   } else if (mode == kPartTraced) {
     w.take<uint32_t>(n + 4);  // carried input indices (a2)
-    w.take<uint32_t>(n + 4);  // lmap
   }
   return w.used + 4096;
 }
@@ -2157,7 +2145,7 @@ static int run_partition(const KeyOf<H>* keys, uint64_t n, const HashParams& hp,
 
 // positions != nullptr: build_traced -- the partition also records its
 // position maps (kPartTraced), k_repart carries every key's input index to
-// the grouped order, and the local build writes positions[p] and lmap[g] = p.
+// the grouped order, and the local build writes positions[p].
 // The workspace then holds the trace hg_intersect_tables reuses.
 template <typename H>
 static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, uint64_t v, const BinLayout& L, uint32_t* offsets,
@@ -2183,13 +2171,12 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
       HG_LAUNCH("hg_part2", kp2, L.grid, kT, smP, st, (const K*)po.out1, hp, L.s, L.nb1, po.c_start, po.tp,
                 po.fine_cursor, edges, nullptr, nullptr, c0, c1);
       HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, (const K*)edges,
-                po.fine_start, L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr, c0 * L.sub, c1 * L.sub);
+                po.fine_start, L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, c0 * L.sub, c1 * L.sub);
     }
   }
-  uint32_t *a2 = nullptr, *lmap = nullptr;
+  uint32_t* a2 = nullptr;
   if (traced) {
     a2 = ws.take<uint32_t>(n + 4);
-    lmap = ws.take<uint32_t>(n + 4);
     if (!ws.ok()) return set_error(HG_ERR_CONFIG, "binned workspace too small for a traced build");
     const size_t smR = (size_t)kUnpStaged * 4;
     HG_SET_SMEM((k_repart<1>), (int)smR);
@@ -2207,11 +2194,11 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   if (traced) {
     HG_SET_SMEM((k_local_build_p<H, true>), (int)smC);
     HG_LAUNCH("hg_local_build_traced", (k_local_build_p<H, true>), num_sms(), LocalPShape<K>::kThreads, smC, st, grouped,
-              po.fine_start, L.nfine, hp, L.s, v, offsets, edges, a2, positions, lmap);
+              po.fine_start, L.nfine, hp, L.s, v, offsets, edges, a2, positions);
   } else if (!grouped_sched) {
     HG_SET_SMEM((k_local_build_p<H>), (int)smC);
     HG_LAUNCH("hg_local_build", k_local_build_p<H>, num_sms(), LocalPShape<K>::kThreads, smC, st, grouped, po.fine_start,
-              L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr, nullptr);
+              L.nfine, hp, L.s, v, offsets, edges, nullptr, nullptr);
   }
   // oversized fine bins (hg_bigbin.cuh), in chunks over the whole grid: with
   // two levels (untraced) their keys sit in edges (in place), so the count
@@ -2223,10 +2210,10 @@ static int build_impl(const KeyOf<H>* keys, uint64_t n, const HashParams& hp, ui
   HG_SET_SMEM((k_big_count<H>), (int)smBig);
   const uint32_t* huge_list = po.big_list + L.nfine - 1;  // grows downwards (k_starts)
   HG_LAUNCH("hg_big_count", k_big_count<H>, num_sms(), 1024, smBig, st, grouped, (K*)po.out1, copy, po.fine_start,
-            po.big_list, huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges, a2, positions, lmap);
+            po.big_list, huge_list, po.big_count, po.big_cp, po.big_done, hp, L.s, v, offsets, edges, a2, positions);
   HG_SET_SMEM((k_big_place<H>), (int)smBig);
   HG_LAUNCH("hg_big_place", k_big_place<H>, num_sms(), 1024, smBig, st, (const K*)src, po.fine_start, huge_list,
-            po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges, a2, positions, lmap);
+            po.big_count, po.big_cp, po.big_done + L.nfine + 1, hp, L.s, v, offsets, edges, a2, positions);
   return HG_OK;
 }
 
@@ -2310,43 +2297,6 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
     out[i] = src[__ldcs(idx + i)];
 }
 
-// Counts in query-table slot order -> grouped order, one CTA per fine bin of
-// the trace's layout: a bin's slots and its grouped keys share the range
-// [fine_start[f], fine_start[f+1]), so the bin's counts are staged in smem and
-// read back through lmap (coalesced in and out); bins above the smem
-// capacity gather from global memory.
-constexpr uint32_t kPermCap = 20480;
-
-__global__ void __launch_bounds__(512) k_perm_bins(const uint32_t* __restrict__ src, const uint32_t* __restrict__ lmap,
-                                                   const uint32_t* __restrict__ fine_start, uint32_t* __restrict__ out) {
-  extern __shared__ uint32_t sm[];  // kPermCap
-  constexpr int U = 8;  // elements per thread per round, loads first
-  const uint32_t f = blockIdx.x;
-  const uint32_t lo = fine_start[f], hi = fine_start[f + 1], cnt = hi - lo;
-  const uint32_t step = U * blockDim.x;
-  if (cnt <= kPermCap) {
-    for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += step) {
-      uint32_t x[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) x[u] = i0 + u * blockDim.x < cnt ? __ldcs(src + lo + i0 + u * blockDim.x) : 0u;
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        if (i0 + u * blockDim.x < cnt) sm[i0 + u * blockDim.x] = x[u];
-    }
-    __syncthreads();
-    for (uint32_t i0 = threadIdx.x; i0 < cnt; i0 += step) {
-      uint32_t x[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) x[u] = i0 + u * blockDim.x < cnt ? __ldcs(lmap + lo + i0 + u * blockDim.x) - lo : 0u;
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        if (i0 + u * blockDim.x < cnt) out[lo + i0 + u * blockDim.x] = sm[x[u]];
-    }
-  } else {
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[lo + i] = src[lmap[lo + i]];
-  }
-}
-
 __global__ void k_scatter_pos(const uint32_t* __restrict__ src, const uint32_t* __restrict__ pos, uint64_t n,
                               uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -2354,11 +2304,15 @@ __global__ void k_scatter_pos(const uint32_t* __restrict__ src, const uint32_t* 
 }
 
 // intersect_tables (query.py:120-179) over a query table that is already
-// grouped by bucket: its fine-bin slices are the probe's query ranges, so no
-// partition runs.  Counts come out in query-table slot order and go back to
-// query order either through the trace of the hg_build that produced the
-// query table with positions (lmap -> grouped order -> k_unpart x 2, all
-// streaming) or, for foreign positions, by scatter.
+// grouped by bucket, so no partition runs.  With the trace of the hg_build
+// that produced the query table with positions, the probe reads the trace's
+// grouped query keys -- exactly what hg_query's partition leaves (grouped by
+// fine bin, in the order the position maps undo) -- and the counts go back to
+// query order through the maps (k_unpart x 2), as in the fused query: at the
+// table's probe layout when the trace's fine bins nest in it, else at the
+// trace's own coarser layout (slices above the smem capacity take the map /
+// hash-table paths).  Without a trace (foreign positions) the query table's
+// fine-bin slices are probed and the counts scatter through positions.
 template <typename H>
 static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t n_table, const uint32_t* q_off,
                        const KeyOf<H>* q_edges, const uint32_t* positions, uint64_t q, const HashParams& hp, uint64_t v,
@@ -2368,49 +2322,38 @@ static int tables_impl(const uint32_t* t_off, const KeyOf<H>* t_edges, uint64_t 
   uint32_t* q_start = ws.take<uint32_t>(Lp.nfine + 1);
   unsigned long long* plan = ws.take<unsigned long long>(kPlanWords);
   ProbeBufs pb;
-  probe_alloc<K>(q, Lp, n_table, ws, &pb);
-  uint32_t* vals = ws.take<uint32_t>(q + 4);
+  probe_alloc<K>(q, Lp, n_table, ws, &pb);  // (a coarser trace layout has fewer fine bins: these fit it too)
   uint32_t* level1 = ws.take<uint32_t>(q + 4);
   if (!ws.ok()) return set_error(HG_ERR_CONFIG, "intersect_tables workspace too small (%zu < %zu)", ws.cap, ws.used);
+  HG_CHECK_CUDA(cudaMemsetAsync(plan, 0, kPlanWords * 8, st));
+  if (!trace) {
+    HG_LAUNCH("hg_qstart", k_qstart, (Lp.nfine + 256) / 256, 256, 0, st, q_off, Lp.nfine, Lp.s, v, q_start);
+    int rc = probe_stage<H>(t_off, t_edges, q_edges, q_start, q, hp, v, Lp, plan, pb, agg, st);
+    if (rc) return rc;
+    HG_LAUNCH("hg_scatter_pos", k_scatter_pos, num_sms() * 8, 256, 0, st, pb.mult_bo, positions, q, mult);
+    return HG_OK;
+  }
+  // re-derive the trace's buffers: the same carve-up as the traced build
   PartOut tpo{};
-  uint32_t* lmap = nullptr;
-  if (trace) {  // re-derive the trace's buffers: the same carve-up as the traced build
+  {
     Workspace tw{(char*)trace, trace_bytes, 0};
     uint32_t *fc, *fcur;
     K* out2;
     part_alloc<K>(q, *Lt, kPartTraced, nullptr, tw, &tpo, &fc, &fcur, &out2);
     tw.take<uint32_t>(q + 4);  // a2
-    lmap = tw.take<uint32_t>(q + 4);
     if (!tw.ok()) return set_error(HG_ERR_CONFIG, "trace buffer too small (%zu < %zu)", tw.cap, tw.used);
   }
-  HG_CHECK_CUDA(cudaMemsetAsync(plan, 0, kPlanWords * 8, st));
-  // A trace grouped at the probe's layout or a finer one holds the query
-  // keys exactly as hg_query's partition leaves them (grouped by fine bin, in
-  // the order the position maps undo): the probe reads them there and its
-  // counts go straight back through the maps, as in the fused query.
-  const bool grouped = trace && Lt->s <= Lp.s;
+  const BinLayout& L = *Lt;
   int rc;
-  if (grouped) {
-    HG_LAUNCH("hg_qstart", k_qstart_nested, (Lp.nfine + 256) / 256, 256, 0, st, tpo.fine_start, Lt->nfine, Lp.nfine,
-              Lp.s - Lt->s, q_start);
+  if (L.s <= Lp.s) {
+    HG_LAUNCH("hg_qstart", k_qstart_nested, (Lp.nfine + 256) / 256, 256, 0, st, tpo.fine_start, L.nfine, Lp.nfine,
+              Lp.s - L.s, q_start);
     rc = probe_stage<H>(t_off, t_edges, (const K*)tpo.grouped, q_start, q, hp, v, Lp, plan, pb, agg, st);
   } else {
-    HG_LAUNCH("hg_qstart", k_qstart, (Lp.nfine + 256) / 256, 256, 0, st, q_off, Lp.nfine, Lp.s, v, q_start);
-    rc = probe_stage<H>(t_off, t_edges, q_edges, q_start, q, hp, v, Lp, plan, pb, agg, st);
+    rc = probe_stage<H>(t_off, t_edges, (const K*)tpo.grouped, tpo.fine_start, q, hp, v, L, plan, pb, agg, st);
   }
   if (rc) return rc;
-  const int g = num_sms() * 8;
-  if (!trace) {
-    HG_LAUNCH("hg_scatter_pos", k_scatter_pos, g, 256, 0, st, pb.mult_bo, positions, q, mult);
-    return HG_OK;
-  }
-  const BinLayout& L = *Lt;
-  if (grouped) {
-    vals = pb.mult_bo;  // already in grouped order
-  } else {
-    HG_SET_SMEM((k_perm_bins), (int)(kPermCap * 4));
-    HG_LAUNCH("hg_perm_bins", k_perm_bins, L.nfine, 512, kPermCap * 4, st, pb.mult_bo, lmap, tpo.fine_start, vals);
-  }
+  uint32_t* vals = pb.mult_bo;  // counts in grouped order
   const size_t smR = unpart_smem();
   uint32_t* l1 = vals;
   if (L.two_level) {
@@ -2432,7 +2375,6 @@ size_t binned_tables_ws_bytes(uint64_t q, const BinLayout& Lp, int key_bits, uin
   ProbeBufs pb;
   if (key_bits == 32) probe_alloc<uint32_t>(q, Lp, n_table, w, &pb);
   else probe_alloc<uint64_t>(q, Lp, n_table, w, &pb);
-  w.take<uint32_t>(q + 4);
   w.take<uint32_t>(q + 4);
   return w.used + 4096;
 }

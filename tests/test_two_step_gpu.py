@@ -2,9 +2,10 @@
 
 build_query_table (query.py:84-95) runs a traced binned build: positions come
 from the partition's own position maps (k_repart), not from global atomics;
-intersect_tables (query.py:120-179) probes the query table's fine-bin slices
-directly and returns the counts to query order through the trace (or, for
-positions it did not produce, by scatter).  Parity: the same multiplicities
+intersect_tables (query.py:120-179) probes the trace's grouped query keys and
+returns the counts to query order through the trace's position maps (or, for
+positions it did not produce, probes the query table's fine-bin slices and
+scatters).  Parity: the same multiplicities
 and matched / total / comparisons as the oracle's two-step query, positions a
 permutation with keys[positions] == the table's keys.
 """
@@ -87,9 +88,20 @@ def test_build_traced_binned_positions():
 @pytest.mark.parametrize("log2_t,log2_q", [(18, 21), (21, 17), (20, 20)])
 def test_two_step_layouts(log2_t, log2_q):
     """Query tables larger than the table (the trace's fine bins nest inside
-    the probe's: the probe reads the trace's grouped keys), smaller (coarser
-    trace: the query table's own slices are probed and permuted back), and
-    equal (same layout)."""
+    the probe's), smaller and equal: the probe reads the trace's grouped keys
+    at the table's probe layout (at C = 1 both pick the same fine bins)."""
     keys = O.generate_keys(log2_t, 1 << log2_t, 0)
     queries = O.generate_keys(log2_t, 1 << log2_q, 0x51)
     two_step(keys, queries, 1 << log2_t)
+
+
+@pytest.mark.parametrize("log2_q", [15, 17])
+def test_two_step_coarser_trace(log2_q):
+    """A dense table (4 keys per bucket: smaller fine bins) with a sparser
+    query table: the trace's fine bins are coarser than the table's probe
+    layout, so the probe runs at the trace's layout over its grouped keys
+    (table slices above the smem capacity take the map / hash-table paths)."""
+    n = 1 << 20
+    keys = O.generate_keys(20, n, 0)
+    queries = np.concatenate([O.generate_keys(20, (1 << log2_q) - 1000, 0x51), keys[:1000]])
+    two_step(keys, queries, n // 4)
