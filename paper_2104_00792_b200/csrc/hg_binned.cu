@@ -2291,12 +2291,6 @@ __global__ void k_qstart_nested(const uint32_t* __restrict__ fs, uint32_t nfine_
   if (f <= nfine_p) q_start[f] = fs[min((uint64_t)f << d, (uint64_t)nfine_t)];
 }
 
-__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n,
-                             uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = src[__ldcs(idx + i)];
-}
-
 __global__ void k_scatter_pos(const uint32_t* __restrict__ src, const uint32_t* __restrict__ pos, uint64_t n,
                               uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
