@@ -291,8 +291,19 @@ k_hist(const KeyOf<H>* __restrict__ keys, uint64_t n, HashParams hp, int s, uint
   }
   for (uint32_t i = threadIdx.x; i < nf; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
-  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  uint64_t lo = (uint64_t)blockIdx.x * chunk;
   const uint64_t hi = min(n, lo + chunk);
+  {
+    // keys that are a view at an offset (e.g. one virtual shard's rows): the
+    // < 16 / sizeof(K) keys before the next 16-byte boundary one by one, the
+    // rest with vector loads
+    const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(keys + lo) & 15);
+    if (mis && (mis % sizeof(K)) == 0 && lo < hi) {
+      const uint64_t head = min(hi - lo, (uint64_t)((16 - mis) / sizeof(K)));
+      if (threadIdx.x < head) hist_add(s_h, f_lo, nf, fine_of<H>(keys[lo + threadIdx.x], hp, s));
+      lo += head;
+    }
+  }
   if (sizeof(K) == 8 && lo < hi && ((reinterpret_cast<uintptr_t>(keys + lo) & 15) == 0)) {
     const uint4* p = reinterpret_cast<const uint4*>(keys + lo);
     const uint64_t nv = (hi - lo) / 2;

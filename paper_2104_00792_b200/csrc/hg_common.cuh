@@ -82,6 +82,8 @@ struct HashParams {
   uint32_t seed;
   int kind;        // 0 murmur, 1 identity
   int mode;        // kMask / kFastmod / kNone / kGeneric64
+  uint32_t m32;    // kFastmod, 32-bit values: Granlund-Montgomery multiplier for floor(x / v)
+  uint32_t sh2;    // ... and its second shift (the first is 1)
 };
 
 enum { kMask = 0, kFastmod = 1, kNone = 2, kGeneric64 = 3 };
@@ -100,6 +102,12 @@ inline HashParams make_hash_params(int kind, uint32_t seed, uint64_t v, int key_
   } else if (v <= 0xFFFFFFFFull) {
     hp.mode = kFastmod;
     hp.magic = UINT64_MAX / v + 1;
+    // floor(x / v) = (t + ((x - t) >> 1)) >> (l - 1), t = umulhi(x, m32), for
+    // every 32-bit x (v not a power of two here, so 2 < v < 2^32 and l >= 2)
+    int l = 0;
+    while ((1ull << l) < v) l++;
+    hp.m32 = (uint32_t)((((1ull << l) - v) << 32) / v + 1);
+    hp.sh2 = (uint32_t)(l - 1);
   } else {
     hp.mode = kGeneric64;
   }
@@ -129,6 +137,20 @@ __device__ __forceinline__ uint32_t fastmod_u32(uint32_t x, uint64_t magic, uint
   return (uint32_t)__umul64hi(low, (uint64_t)d);
 }
 
+// x mod d for 32-bit x and a non-power-of-two d < 2^32 by division with an
+// invariant multiplier (Granlund & Montgomery): two integer multiplies and
+// five ALU operations, where Lemire's 64-bit fastmod issues five wide
+// multiplies (the multiply pipe is what the build kernels' hashing waits on).
+__host__ __device__ __forceinline__ uint32_t mod_gm32(uint32_t x, uint32_t m, uint32_t sh2, uint32_t d) {
+#ifdef __CUDA_ARCH__
+  const uint32_t t = __umulhi(x, m);
+#else
+  const uint32_t t = (uint32_t)(((uint64_t)x * m) >> 32);
+#endif
+  const uint32_t q = (t + ((x - t) >> 1)) >> sh2;
+  return x - q * d;
+}
+
 // x mod d for any 64-bit x: q = floor(x * m / 2^64) with m = floor((2^64-1)/d)
 // undershoots floor(x/d) by at most 2, so two conditional subtractions finish.
 __device__ __forceinline__ uint64_t barrett_mod64(uint64_t x, uint64_t m, uint64_t d) {
@@ -156,7 +178,7 @@ __device__ __forceinline__ uint64_t hash_mod(K key, const HashParams& hp) {
     case kNone:
       return x;
     case kFastmod:
-      if (sizeof(K) == 4) return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
+      if (sizeof(K) == 4) return mod_gm32((uint32_t)x, hp.m32, hp.sh2, (uint32_t)hp.v);
       return barrett_mod64(x, hp.magic64, hp.v);
     default:
       return barrett_mod64(x, hp.magic64, hp.v);
@@ -184,7 +206,7 @@ struct Hasher {
     } else if constexpr (MODE == kNone) {
       return (uint32_t)x;
     } else if constexpr (MODE == kFastmod && sizeof(K) == 4) {
-      return fastmod_u32((uint32_t)x, hp.magic, (uint32_t)hp.v);
+      return mod_gm32((uint32_t)x, hp.m32, hp.sh2, (uint32_t)hp.v);
     } else {
       return (uint32_t)barrett_mod64(x, hp.magic64, hp.v);
     }
