@@ -256,3 +256,36 @@ def test_c1_exact_vs_oracle():
     assert np.array_equal(res.multiplicities, mult)
     assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
     assert matched == 10_601_263  # SURVEY §8(d), measured with the reference
+
+
+@pytest.mark.parametrize("v", [(1 << 32) - 1, (1 << 31) + 1, (1 << 31) + 12345, 3, 5, 641, (1 << 20) * 3 + 1])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_hash_mod_extreme_ranges(v, kind):
+    """hash mod V for non-power-of-two V through the invariant-multiplier
+    reduction (hg_common.cuh mod_gm32): the largest 32-bit V, V just above 2^31
+    (the second shift at its maximum), tiny V; the inputs include the ends of
+    the 32-bit range (identity hash: the reduced value is the key itself)."""
+    rng = np.random.default_rng(v % 1000003 + kind)
+    keys = np.concatenate([rng.integers(0, 1 << 32, size=(1 << 20) - 6, dtype=np.uint64),
+                           np.array([0, 1, v - 1, v % (1 << 32), 0xFFFFFFFE, 0xFFFFFFFF], dtype=np.uint64)]
+                          ).astype(np.uint32)
+    got = hg.hash_array(fam(kind, 99), keys, v)
+    assert np.array_equal(got, O.hash_keys(kind, 99, keys, v).astype(np.int64))
+
+
+@pytest.mark.parametrize("v,kind", [((1 << 20) * 3, 0), ((1 << 20) + 1, 1), ((1 << 21) - 1, 0), (12345, 1)])
+def test_non_power_of_two_ranges_vs_oracle(v, kind):
+    """Binned and direct builds and queries at non-power-of-two ranges."""
+    n = 1 << 20
+    rng = np.random.default_rng(v)
+    keys = np.concatenate([rng.integers(0, 1 << 32, size=n - 4, dtype=np.uint64),
+                           np.array([0, 1, 0xFFFFFFFE, 0xFFFFFFFF], dtype=np.uint64)]).astype(np.uint32)
+    queries = np.concatenate([keys[::5], rng.integers(0, 1 << 32, size=n // 5, dtype=np.uint64).astype(np.uint32)])
+    f = fam(kind, 99)
+    table = hg.build(keys, 1.0, f, hash_range=v)
+    off, placed, _ = O.build_csr(keys, v, kind, 99, workers=8)
+    assert_table_equal(table, off, placed)
+    res = hg.intersect(table, queries)
+    mult, matched, total, comp, hv = O.query(off, placed, queries, kind, 99, workers=8)
+    assert np.array_equal(res.multiplicities, mult)
+    assert (res.matched_positions, res.total_matches, res.comparisons) == (matched, total, comp)
