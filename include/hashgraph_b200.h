@@ -151,6 +151,15 @@ HG_API int hg_reorganize(const void* keys, uint64_t n, int key_bits, int kind, u
                   uint64_t hash_range, uint64_t bin_size, const int64_t* splits, uint32_t shards,
                   uint64_t* row_offsets, void* grouped, uint32_t* order, uint64_t* search_steps,
                   void* workspace, size_t workspace_bytes, void* stream);
+/* Values per reorganized key back to input order: out[i] = vals[slot of key i]
+ * for the rows hg_reorganize produced from these very keys (same hash, plan and
+ * splits), whose `workspace` still holds that call's tile bases -- the query
+ * answers of query_sharded (multishard.py:510-535) returned with coalesced
+ * stores instead of a scatter through `order`. */
+HG_API int hg_reorganize_gather(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed,
+                         uint64_t hash_range, uint64_t bin_size, const int64_t* splits, uint32_t shards,
+                         const uint64_t* row_offsets, const uint32_t* vals, uint32_t* out, const void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* Phase 2 + Phase 3 fused over peer memory (one process per GPU; the receive
  * buffers are symmetric allocations mapped into every rank over NVLink /

@@ -51,6 +51,8 @@ SIGNATURES = {
     "hg_reorganize_workspace_size": (_c_size, [_c_u64, _c_u32]),
     "hg_reorganize": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_u64, _c_ptr, _c_u32, _c_ptr,
                                _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_size, _c_ptr]),
+    "hg_reorganize_gather": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_u64, _c_ptr, _c_u32, _c_ptr,
+                                      _c_ptr, _c_ptr, _c_ptr, _c_size, _c_ptr]),
     "hg_reorganize_count": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_u64, _c_ptr, _c_u32, _c_ptr,
                                      _c_ptr, _c_ptr, _c_size, _c_ptr]),
     "hg_reorganize_place_peers": (_c_int, [_c_ptr, _c_u64, _c_int, _c_int, _c_u32, _c_u64, _c_u64, _c_ptr, _c_u32,

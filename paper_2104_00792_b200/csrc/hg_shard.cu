@@ -227,13 +227,19 @@ __global__ void k_reorg_rows(const unsigned long long* __restrict__ totals, uint
 // destination rank's receive buffer (dest_ptrs[d], peer memory mapped over
 // NVLink / NVSwitch) at dest_base[d] + (its stable rank in row d); `order`
 // still records the input index at the local grouped position.
-template <typename K, bool kPeer>
+//
+// kGather (hg_reorganize_gather): the same stable slots, read instead of
+// written -- gout[i] = gvals[slot of input key i] returns per-row values to
+// input order with coalesced stores (a scatter through `order` writes each
+// row's values at 1/P density across the whole output).
+template <typename K, bool kPeer, bool kGather = false>
 __global__ void __launch_bounds__(kReorgWarps * 32)
 k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams bin,
               const long long* __restrict__ splits, uint32_t shards,
               const uint32_t* __restrict__ tile_base, const unsigned long long* __restrict__ row_offsets,
               K* __restrict__ grouped, uint32_t* __restrict__ order,
-              const unsigned long long* __restrict__ dest_ptrs, const unsigned long long* __restrict__ dest_base) {
+              const unsigned long long* __restrict__ dest_ptrs, const unsigned long long* __restrict__ dest_base,
+              const uint32_t* __restrict__ gvals = nullptr, uint32_t* __restrict__ gout = nullptr) {
   extern __shared__ unsigned char s_raw[];
   long long* s_splits = reinterpret_cast<long long*>(s_raw);
   unsigned long long* s_base = reinterpret_cast<unsigned long long*>(s_splits + shards + 1);
@@ -284,6 +290,7 @@ k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
   // place: a round's lanes with the same destination take consecutive slots
   // in lane order after the warp's cursor (stable: rounds, then lanes, in
   // input order)
+  unsigned long long gsl[kGather ? kReorgPerLane : 1];
 #pragma unroll
   for (int r = 0; r < kReorgPerLane; r++) {
     const uint32_t d = dv[r];
@@ -296,10 +303,23 @@ k_reorg_place(const K* __restrict__ keys, uint64_t n, HashParams hp, DivParams b
     if (ok) {
       const uint32_t rank = cur + __popc(peers & lt);
       const unsigned long long slot = s_base[d] + rank;
-      if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[s_rbase[d] + rank] = kv[r];
-      else grouped[slot] = kv[r];
-      if (order) order[slot] = (uint32_t)(wbase + r * 32 + lane);
+      if (kGather) {
+        gsl[r % (kGather ? kReorgPerLane : 1)] = slot;  // loaded after the loop: all rounds' gathers in flight at once
+      } else {
+        if (kPeer) reinterpret_cast<K*>(dest_ptrs[d])[s_rbase[d] + rank] = kv[r];
+        else grouped[slot] = kv[r];
+        if (order) order[slot] = (uint32_t)(wbase + r * 32 + lane);
+      }
     }
+  }
+  if (kGather) {
+    uint32_t gv[kGather ? kReorgPerLane : 1];
+#pragma unroll
+    for (int r = 0; r < kReorgPerLane; r++)
+      if (dv[r] != 0xffffffffu) gv[r % (kGather ? kReorgPerLane : 1)] = __ldcs(gvals + gsl[r % (kGather ? kReorgPerLane : 1)]);
+#pragma unroll
+    for (int r = 0; r < kReorgPerLane; r++)
+      if (dv[r] != 0xffffffffu) gout[wbase + r * 32 + lane] = gv[r % (kGather ? kReorgPerLane : 1)];
   }
   if (kPeer) __threadfence_system();  // peer stores ordered before the barrier that publishes them
 }
@@ -567,6 +587,28 @@ static int reorg_place(const void* keys, uint64_t n, int key_bits, const HashPar
   return HG_OK;
 }
 
+// Per-row values back to input order (kGather): the tile bases of the
+// count pass that produced row_offsets are still in the workspace.
+static int reorg_gather(const void* keys, uint64_t n, int key_bits, const HashParams& hp, const DivParams& dp,
+                        const int64_t* splits, uint32_t shards, const uint32_t* tile_counts, const uint64_t* row_offsets,
+                        const uint32_t* vals, uint32_t* out, cudaStream_t s) {
+  const uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  const size_t smem_p = 8 * (shards + 1) + 8 * shards + 4 * kReorgWarps * shards;
+  const auto* ro = (const unsigned long long*)row_offsets;
+  if (key_bits == 32) {
+    HG_SET_SMEM((k_reorg_place<uint32_t, false, true>), (int)smem_p);
+    HG_LAUNCH("hg_reorg_gather", (k_reorg_place<uint32_t, false, true>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
+              (const uint32_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, nullptr, nullptr,
+              nullptr, nullptr, vals, out);
+  } else {
+    HG_SET_SMEM((k_reorg_place<uint64_t, false, true>), (int)smem_p);
+    HG_LAUNCH("hg_reorg_gather", (k_reorg_place<uint64_t, false, true>), (unsigned)tiles, kReorgWarps * 32, smem_p, s,
+              (const uint64_t*)keys, n, hp, dp, (const long long*)splits, shards, tile_counts, ro, nullptr, nullptr,
+              nullptr, nullptr, vals, out);
+  }
+  return HG_OK;
+}
+
 static int reorg_check(int key_bits, int kind, uint64_t hash_range, uint32_t shards, uint64_t bin_size, uint64_t n) {
   int rc = check_hash(key_bits, kind, hash_range);
   if (rc) return rc;
@@ -671,6 +713,23 @@ int hg_reorganize(const void* keys, uint64_t n, int key_bits, int kind, uint32_t
   if (rc) return rc;
   return reorg_place<false>(keys, n, key_bits, hp, dp, splits, shards, tile_counts, row_offsets, grouped, order,
                             nullptr, nullptr, s);
+}
+
+int hg_reorganize_gather(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,
+                         uint64_t bin_size, const int64_t* splits, uint32_t shards, const uint64_t* row_offsets,
+                         const uint32_t* vals, uint32_t* out, const void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  int rc = reorg_check(key_bits, kind, hash_range, shards, bin_size, n);
+  if (rc) return rc;
+  if (!n) return HG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t tiles = (n + kReorgTile - 1) / kReorgTile;
+  Workspace ws{(char*)const_cast<void*>(workspace), workspace_bytes, 0};
+  const uint32_t* tile_counts = ws.take<uint32_t>(tiles * shards);  // the carve-up of hg_reorganize
+  if (!ws.ok()) return set_error(HG_ERR_CONFIG, "reorganize workspace too small");
+  HashParams hp = make_hash_params(kind, seed, hash_range, key_bits);
+  DivParams dp = make_div_params(bin_size);
+  return reorg_gather(keys, n, key_bits, hp, dp, splits, shards, tile_counts, row_offsets, vals, out, s);
 }
 
 int hg_reorganize_count(const void* keys, uint64_t n, int key_bits, int kind, uint32_t seed, uint64_t hash_range,

@@ -313,8 +313,9 @@ def split_plan_device(counts, bins_g, total, shards):
 
 
 def reorganize_device(keys_dev, hash_range, bin_size, splits_dev, shards, family, key_bits=32,
-                      want_order=False, steps=None):
-    """Phase 2 on device: (row_offsets int64[P+1] device, grouped keys, order u32 | None)."""
+                      want_order=False, steps=None, keep_workspace=False):
+    """Phase 2 on device: (row_offsets int64[P+1] device, grouped keys, order u32 | None)
+    (+ the workspace, whose tile bases hg_reorganize_gather reuses, with keep_workspace)."""
     t = D.torch()
     n = keys_dev.numel()
     kind, seed = family_code(family)
@@ -325,6 +326,8 @@ def reorganize_device(keys_dev, hash_range, bin_size, splits_dev, shards, family
     _lib.call("hg_reorganize", D.ptr(keys_dev), n, key_bits, kind, seed, hash_range, bin_size, D.ptr(splits_dev),
               shards, D.ptr(rows), D.ptr(grouped), D.ptr(order), D.ptr(steps), D.ptr(ws), ws.numel(),
               D.stream_ptr())
+    if keep_workspace:
+        return rows, grouped, order, ws
     return rows, grouped, order
 
 
@@ -651,8 +654,9 @@ def query_sharded_timed(table: ShardedHashGraph, queries, worker_count: int = 1)
 
 def _query_sharded(table: ShardedHashGraph, queries, worker_count: int, timed: bool):
     """Queries are routed on shard 0's device with the table's plan (stable
-    rows + the input order), each row is answered on its shard's device and
-    the uint32 answers come back to be scattered into input order there."""
+    rows), each row is answered on its shard's device into its slice of one
+    grouped answer array, and hg_reorganize_gather returns the answers to
+    input order there (recomputing each query's row slot, coalesced stores)."""
     if worker_count < 1:
         raise ConfigError(f"worker count must be >= 1, got {worker_count}")
     t = D.require_cuda()
@@ -665,10 +669,12 @@ def _query_sharded(table: ShardedHashGraph, queries, worker_count: int, timed: b
         nq = q.numel()
         ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
-        rows, grouped, order = reorganize_device(q, plan.hash_range, plan.bin_size, plan.splits_device(), p,
-                                                 table.family, key_bits, want_order=True)
+        splits_dev = plan.splits_device()
+        rows, grouped, _, rws = reorganize_device(q, plan.hash_range, plan.bin_size, splits_dev, p, table.family,
+                                                  key_bits, keep_workspace=True)
         rows_h = rows.cpu().numpy()
         mult = t.zeros(nq, dtype=t.int32, device=D.device())
+        answers = t.zeros(nq + 4, dtype=t.int32, device=D.device())  # grouped (row) order
         agg = t.zeros(3, dtype=t.int64, device=D.device())
         hash_values = 0
         ev[1].record()
@@ -680,8 +686,13 @@ def _query_sharded(table: ShardedHashGraph, queries, worker_count: int, timed: b
             m_d, a_d = query_device(shard, grouped[lo:hi])  # on the shard's device
             if m_d.device != mult.device:
                 m_d, a_d = m_d.to(mult.device), a_d.to(mult.device)
-            _lib.call("hg_scatter_u32", D.ptr(m_d), D.ptr(order[lo:hi]), hi - lo, D.ptr(mult), D.stream_ptr())
+            answers[lo:hi].copy_(m_d)
             agg += a_d
+        if nq:
+            kind, seed = family_code(table.family)
+            _lib.call("hg_reorganize_gather", D.ptr(q), nq, key_bits, kind, seed, plan.hash_range, plan.bin_size,
+                      D.ptr(splits_dev), p, D.ptr(rows), D.ptr(answers), D.ptr(mult), D.ptr(rws), rws.numel(),
+                      D.stream_ptr())
         ev[2].record()
     result = QueryResult(mult, agg, hash_values)
     if not timed:

@@ -26,3 +26,12 @@ acc = defaultdict(float); cnt = defaultdict(int)
 for name, ms in _lib.timing_collect(1 << 14):
     acc[name] += ms; cnt[name] += 1
 print("query wall", (t1 - t0) * 1e3, "kernels", " ".join(f"{k} {v:.3f}x{cnt[k]}" for k, v in sorted(acc.items(), key=lambda kv: -kv[1])))
+ts = []
+for _ in range(5):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = hg.query_sharded(table, qs)
+    _ = res.matched_positions
+    torch.cuda.synchronize()
+    ts.append(1e3 * (time.perf_counter() - t0))
+print("query wall x5 (ms)", " ".join(f"{x:.2f}" for x in ts))
